@@ -1,0 +1,228 @@
+"""ctypes wrapper of the fp64 CPU ORACLE (oracle/dinr_oracle.c).
+
+TEST INFRASTRUCTURE ONLY: only tests/, __graft_entry__.smoke() and bench.py's
+cpu_baseline / ``--impl reference`` legs may import this module.  The product package
+(paper_2404_19075_b200) never imports it; the two share no code.  Inputs come from the
+seeded generators in paper_2404_19075_b200/synth.py, which hold none of the method's
+arithmetic.
+
+Parity pins for every function live in tests/test_oracle_*.py.  The MLP's *values* have
+no paper-printed worked example; they are pinned by closed-form special cases, a
+torch.autograd float64 library reference and central finite differences.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "liboracle.so")
+_SRC = os.path.join(_HERE, "dinr_oracle.c")
+
+
+def build(force: bool = False) -> str:
+    """Compile liboracle.so (gcc, -O2 -ffp-contract=off, OpenMP)."""
+    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < max(
+        os.path.getmtime(_SRC), os.path.getmtime(os.path.join(_HERE, "dinr_oracle.h"))
+    ):
+        subprocess.check_call(
+            ["gcc", "-O2", "-ffp-contract=off", "-fopenmp", "-fPIC", "-shared", "-o", _SO, _SRC, "-lm"]
+        )
+    return _SO
+
+
+class OrGeom(C.Structure):
+    _fields_ = [
+        ("beam", C.c_int32), ("n_rows", C.c_int32), ("n_cols", C.c_int32),
+        ("sub_x", C.c_int32), ("sub_z", C.c_int32), ("n_s", C.c_int32),
+        ("sod", C.c_double), ("odd", C.c_double), ("dx", C.c_double), ("dz", C.c_double),
+        ("cx", C.c_double), ("cz", C.c_double), ("r", C.c_double), ("xs0", C.c_double),
+        ("z_lo", C.c_double), ("z_hi", C.c_double), ("t_lo", C.c_double), ("t_hi", C.c_double),
+    ]
+
+
+class OrField(C.Structure):
+    _fields_ = [("C", C.c_int32), ("L", C.c_int32), ("combine", C.c_int32), ("pad", C.c_int32),
+                ("mu0", C.c_double)]
+
+
+class OrPrim(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("pad", C.c_int32), ("value", C.c_double),
+                ("c0", C.c_double * 3), ("vel", C.c_double * 3), ("a0", C.c_double * 3),
+                ("arate", C.c_double * 3)]
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        _lib = C.CDLL(build())
+        d, i64, i32 = C.POINTER(C.c_double), C.c_int64, C.c_int32
+        pi64 = C.POINTER(C.c_int64)
+        _lib.or_param_count.restype = i64
+        _lib.or_param_count.argtypes = [i32, i32]
+        _lib.or_rotate_point.argtypes = [C.c_double] * 4 + [d, d]
+        _lib.or_fov_delta_bounds.argtypes = [d, d, C.c_double, C.c_double, d, d]
+        _lib.or_rays.argtypes = [C.POINTER(OrGeom), d, i64, pi64, i64, d]
+        _lib.or_grff.argtypes = [i32, d, d, i64, d]
+        _lib.or_mlp_eval.argtypes = [C.POINTER(OrField), d, d, d, i64, d]
+        _lib.or_mlp_grad.argtypes = [C.POINTER(OrField), d, d, d, d, i64, d]
+        _lib.or_project.argtypes = [C.POINTER(OrGeom), d, d, i64, C.POINTER(OrField), d, d, pi64, i64, d, d]
+        _lib.or_project_and_grad.argtypes = [C.POINTER(OrGeom), d, d, i64, C.POINTER(OrField), d, d, pi64, i64, d, d]
+        _lib.or_project_analytic.argtypes = [C.POINTER(OrGeom), d, d, i64, i32, C.POINTER(OrPrim), i32, pi64, i64, d, d]
+        _lib.or_project_exact.argtypes = [C.POINTER(OrGeom), d, d, i64, i32, C.POINTER(OrPrim), i32, pi64, i64, d, d]
+        _lib.or_line_integral_exact.restype = C.c_double
+        _lib.or_line_integral_exact.argtypes = [C.POINTER(OrPrim), i32, d, d, C.c_double, C.c_double, C.c_double]
+    return _lib
+
+
+def _dp(a):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def _f64(a):
+    return np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+
+
+def _i64(a):
+    return np.ascontiguousarray(np.asarray(a, dtype=np.int64))
+
+
+_BEAM = {"parallel": 0, "fan": 1, "cone": 2}
+_COMBINE = {"beer": 0, "linear": 1}
+
+
+def geom_struct(g: dict) -> OrGeom:
+    """g: the dict produced by paper_2404_19075_b200.synth (plain numbers)."""
+    return OrGeom(
+        _BEAM[g["beam"]], g["n_rows"], g["n_cols"], g["sub_x"], g["sub_z"], g["n_s"],
+        g["sod"], g["odd"], g["pixel_dx"], g["pixel_dz"], g["offset_cx"], g["offset_cz"],
+        g["fov_radius"], g["rot_center_x"], g["z_lo"], g["z_hi"], g["t_lo"], g["t_hi"],
+    )
+
+
+def field_struct(f: dict) -> OrField:
+    return OrField(f["C"], f["L"], _COMBINE[f.get("combine", "beer")], 0, f["mu0"])
+
+
+def param_count(C_, L):
+    return int(lib().or_param_count(C_, L))
+
+
+def rotate_point(x, y, theta, xs0):
+    xo, yo = C.c_double(), C.c_double()
+    lib().or_rotate_point(x, y, theta, xs0, C.byref(xo), C.byref(yo))
+    return xo.value, yo.value
+
+
+def fov_delta_bounds(src, dst, xs0, r):
+    s, d = _f64(src), _f64(dst)
+    lo, hi = C.c_double(), C.c_double()
+    hit = lib().or_fov_delta_bounds(_dp(s), _dp(d), xs0, r, C.byref(lo), C.byref(hi))
+    return (lo.value, hi.value) if hit else None
+
+
+def rays(g, theta, idx):
+    """-> (n, S, 9) fp64 {o[3], d[3], dmin, dmax, chord}."""
+    th, ix = _f64(theta), _i64(idx)
+    S = g["sub_x"] * g["sub_z"]
+    out = np.zeros((len(ix), S, 9))
+    rc = lib().or_rays(C.byref(geom_struct(g)), _dp(th), len(th), ix.ctypes.data_as(C.POINTER(C.c_int64)), len(ix), _dp(out))
+    return out, rc
+
+
+def grff(B, rbar):
+    Bm = _f64(B)
+    rb = _f64(rbar).reshape(-1, 4)
+    C_ = Bm.shape[0]
+    out = np.zeros((len(rb), 2 * C_))
+    lib().or_grff(C_, _dp(Bm), _dp(rb), len(rb), _dp(out))
+    return out
+
+
+def mlp_eval(f, B, params, rbar):
+    rb = _f64(rbar).reshape(-1, 4)
+    out = np.zeros(len(rb))
+    lib().or_mlp_eval(C.byref(field_struct(f)), _dp(_f64(B)), _dp(_f64(params)), _dp(rb), len(rb), _dp(out))
+    return out
+
+
+def mlp_grad(f, B, params, rbar, u):
+    rb = _f64(rbar).reshape(-1, 4)
+    uu = _f64(u)
+    out = np.zeros(param_count(f["C"], f["L"]))
+    lib().or_mlp_grad(C.byref(field_struct(f)), _dp(_f64(B)), _dp(_f64(params)), _dp(rb), _dp(uu), len(rb), _dp(out))
+    return out
+
+
+def project(g, theta, t, f, B, params, idx):
+    th, tt, ix = _f64(theta), _f64(t), _i64(idx)
+    S = g["sub_x"] * g["sub_z"]
+    fhat, psub = np.zeros(len(ix)), np.zeros((len(ix), S))
+    rc = lib().or_project(C.byref(geom_struct(g)), _dp(th), _dp(tt), len(th), C.byref(field_struct(f)),
+                          _dp(_f64(B)), _dp(_f64(params)), ix.ctypes.data_as(C.POINTER(C.c_int64)), len(ix),
+                          _dp(fhat), _dp(psub))
+    return fhat, psub, rc
+
+
+def project_and_grad(g, theta, t, f, B, params, idx, y):
+    th, tt, ix, yy = _f64(theta), _f64(t), _i64(idx), _f64(y)
+    P = param_count(f["C"], f["L"])
+    grad = np.zeros(P + 1)
+    rc = lib().or_project_and_grad(C.byref(geom_struct(g)), _dp(th), _dp(tt), len(th), C.byref(field_struct(f)),
+                                   _dp(_f64(B)), _dp(_f64(params)), ix.ctypes.data_as(C.POINTER(C.c_int64)), len(ix),
+                                   _dp(yy), _dp(grad))
+    return grad, rc
+
+
+_KIND = {"indicator": 0, "smooth": 1, "gaussian": 2}
+
+
+def prims_array(prims):
+    arr = (OrPrim * max(1, len(prims)))()
+    for q, p in enumerate(prims):
+        arr[q].kind = _KIND[p["kind"]]
+        arr[q].value = p["value"]
+        for k in range(3):
+            arr[q].c0[k] = p["center"][k]
+            arr[q].vel[k] = p.get("velocity", (0, 0, 0))[k]
+            arr[q].a0[k] = p["axes"][k]
+            arr[q].arate[k] = p.get("axes_rate", (0, 0, 0))[k]
+    return arr
+
+
+def project_analytic(g, theta, t, prims, idx, combine="beer"):
+    th, tt, ix = _f64(theta), _f64(t), _i64(idx)
+    S = g["sub_x"] * g["sub_z"]
+    fhat, psub = np.zeros(len(ix)), np.zeros((len(ix), S))
+    rc = lib().or_project_analytic(C.byref(geom_struct(g)), _dp(th), _dp(tt), len(th), _COMBINE[combine],
+                                   prims_array(prims), len(prims), ix.ctypes.data_as(C.POINTER(C.c_int64)), len(ix),
+                                   _dp(fhat), _dp(psub))
+    return fhat, psub, rc
+
+
+def project_exact(g, theta, t, prims, idx, combine="beer"):
+    th, tt, ix = _f64(theta), _f64(t), _i64(idx)
+    S = g["sub_x"] * g["sub_z"]
+    fhat, psub = np.zeros(len(ix)), np.zeros((len(ix), S))
+    rc = lib().or_project_exact(C.byref(geom_struct(g)), _dp(th), _dp(tt), len(th), _COMBINE[combine],
+                                prims_array(prims), len(prims), ix.ctypes.data_as(C.POINTER(C.c_int64)), len(ix),
+                                _dp(fhat), _dp(psub))
+    return fhat, psub, rc
+
+
+def line_integral_exact(prims, o, d, dmin, dmax, t=0.0):
+    return float(lib().or_line_integral_exact(prims_array(prims), len(prims), _dp(_f64(o)), _dp(_f64(d)), dmin, dmax, t))
+
+
+def allreduce_mean(grads):
+    """O13: rank-ordered sum over G ranks, then / G (R16)."""
+    acc = np.zeros_like(np.asarray(grads[0], dtype=np.float64))
+    for g_ in grads:
+        acc = acc + np.asarray(g_, dtype=np.float64)
+    return acc / len(grads)
