@@ -1,0 +1,185 @@
+/*
+ * dinr.h -- C ABI of libdinr.so, the B200 (sm_100a) differentiable forward projector of
+ * arXiv 2404.19075 (DINR, "Distributed Stochastic Optimization of a Neural Representation
+ * Network for Time-Space Tomography Reconstruction").
+ *
+ * Citations: "P:n" = line n of PAPER.md (paper text), "S:n" = line n of SPEC.md,
+ * "R#" = reading # in DESIGN.md ("Readings of the paper").  Everything below is plain C:
+ * pointers, sizes and status codes.  No C++ exception crosses this boundary.
+ *
+ * Ownership and threading:
+ *   - The caller owns every buffer passed in (device "_dev" buffers and host buffers) and
+ *     the CUDA stream; all device work is enqueued on that stream (stream-ordered, async)
+ *     unless a function says it synchronizes.
+ *   - The context owns the per-view table, packed bf16 weights, scratch (ray records,
+ *     per-chunk ray sums, upstream gradients, activation stashes, gradient partials),
+ *     timing events and the NCCL communicator.  One context per device per process; a
+ *     context is not thread-safe (serialize calls on it).
+ *   - Scratch grows on demand with the largest n seen.  Growth allocates; pre-size it with
+ *     one untimed call before capturing a CUDA graph.
+ * Errors:
+ *   - Host-checkable violations return DINR_EINVAL with no side effects.
+ *   - Out-of-range pixel indices (i >= M*N) are seen only on the device: they set a sticky
+ *     device flag, the pixel contributes 0 (fhat = 0, zero gradient), and
+ *     dinr_get_device_status() later returns DINR_ERANGE.
+ *   - A ray that misses the FOV is not an error: p_s = 0 and zero gradient (R21).
+ *   - CUDA / NCCL failures return DINR_ECUDA / DINR_ENCCL; dinr_last_error() has the text.
+ */
+#ifndef DINR_H
+#define DINR_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct dinr_ctx dinr_ctx; /* opaque */
+
+typedef enum {
+  DINR_OK = 0,
+  DINR_EINVAL = 1,  /* invalid argument (host-checked, no side effects)          */
+  DINR_ERANGE = 2,  /* a pixel index was out of range (sticky device flag)        */
+  DINR_ENOMEM = 3,  /* device allocation failed                                   */
+  DINR_ECUDA = 4,   /* CUDA runtime error                                         */
+  DINR_ENCCL = 5,   /* NCCL error                                                 */
+  DINR_ESTATE = 6,  /* call order violated (e.g. weights before geometry)         */
+  DINR_EDEVICE = 7  /* device is not an sm_100 part                               */
+} dinr_status;
+
+typedef enum { DINR_PARALLEL = 0, DINR_FAN = 1, DINR_CONE = 2 } dinr_beam;
+
+/* Sub-ray combine: BEER = per-sub-ray Beer's law averaged over the pixel in transmission
+ * (eq:beerstransavg; default, north_star); LINEAR = average of the line
+ * integrals (eq:beersattenavg / eq:forwmodproj). R5. */
+typedef enum { DINR_BEER = 0, DINR_LINEAR = 1 } dinr_combine;
+
+/* BF16: tcgen05 tensor-core MLP (bf16 operands, fp32 accumulate, fp32 epilogue/head).
+ * FP32_VERIFY: fp32 CUDA-core MLP with accurate sin/cos/exp (the 1e-5 verification mode). */
+typedef enum { DINR_BF16 = 0, DINR_FP32_VERIFY = 1 } dinr_precision;
+
+/* Scanner geometry (all lengths in one unit, e.g. mm; fp64).
+ *   Detector pixel (row j, col i) covers x_d in [-C_x + i*dx, -C_x + (i+1)*dx),
+ *   z_d in [-C_z + j*dz, -C_z + (j+1)*dz) on the plane y = +odd.
+ *   Sources: cone (0,-sod,0); fan (0,-sod,z_d) (R9); parallel (x_d,-sod,z_d) (R10).
+ *   sub_x x sub_z sub-pixel rays to sub-pixel centres, sub-ray s = v*sub_x + u.
+ *   FOV: cylinder (x - rot_center_x)^2 + y^2 <= fov_radius^2, infinite in z.
+ *   samples_per_ray N_s: fixed midpoint rule per ray (R8).
+ *   Normalization box (R11): x -> (x - rot_center_x)/r, y -> y/r,
+ *   z -> (z - (z_lo+z_hi)/2)/((z_hi-z_lo)/2), t -> (t - (t_lo+t_hi)/2)/((t_hi-t_lo)/2);
+ *   a zero-width range maps that coordinate to 0.
+ * Invariants: sod > 0, odd >= 0, pixel pitches > 0, fov_radius > 0,
+ *   fov_radius < sod, sub_x, sub_z >= 1, samples_per_ray >= 32 and a multiple of 32,
+ *   n_rows, n_cols >= 1, z_hi >= z_lo, t_hi >= t_lo. */
+typedef struct {
+  int32_t beam;            /* dinr_beam */
+  int32_t n_rows, n_cols;
+  int32_t sub_x, sub_z;
+  int32_t samples_per_ray;
+  double sod, odd;
+  double pixel_dx, pixel_dz;
+  double offset_cx, offset_cz;
+  double fov_radius, rot_center_x;
+  double z_lo, z_hi;
+  double t_lo, t_hi;
+} dinr_geometry;
+
+/* DINR field network: GRFF with n_freq = C frequencies (width H = 2C), L =
+ * n_layers FC(H->H)+Swish layers, FC head H->1 times mu0 (applied once, R6).
+ * Supported on the BF16 path: H in {64, 128, 256}; FP32_VERIFY: any H <= 256.
+ * mu0 > 0.  combine: dinr_combine.  precision: dinr_precision. */
+typedef struct {
+  int32_t n_freq;
+  int32_t n_layers;
+  int32_t width;           /* must equal 2*n_freq */
+  int32_t combine;
+  int32_t precision;
+  int32_t reserved;        /* 0 */
+  double mu0;
+} dinr_field_desc;
+
+/* Trainable parameter count P = L(H^2+H)+H+1.  Layout of the flat fp32
+ * parameter / gradient vector (D5): for l = 1..L: W_l (H x H row-major [out][in]), b_l (H);
+ * then w_o (H), b_o (1). */
+int64_t dinr_param_count(int32_t n_freq, int32_t n_layers);
+
+/* Create a context on CUDA device `device` (must be compute capability 10.0). */
+dinr_status dinr_create(int device, dinr_ctx **out);
+dinr_status dinr_destroy(dinr_ctx *ctx);
+/* Text of the last error on this context (valid until the next call on it). */
+const char *dinr_last_error(const dinr_ctx *ctx);
+const char *dinr_status_string(dinr_status s);
+
+/* Geometry and view schedule: theta_rad[M] (view angles; source and detector rotate
+ * anticlockwise by theta_k about (x_s0, 0), eq:rotxsk-rotydk P:88-106, R4) and t[M]
+ * (acquisition times, t_i = T_m for every pixel of view m, non-decreasing).
+ * Host arrays, copied before return (synchronous).  cos/sin of theta are taken on the host. */
+dinr_status dinr_set_geometry(dinr_ctx *ctx, const dinr_geometry *g, const double *theta_rad,
+                              const double *t, int64_t M);
+
+/* Field weights: B_dev = GRFF matrix (C x 4 fp32, columns t,z,y,x, frozen, R12);
+ * params_dev = P fp32 trainable parameters (D5 layout).  Packs bf16 tensor-core operands on
+ * `stream` (stream-ordered; the caller may overwrite params_dev after this on the same
+ * stream).  Requires dinr_set_geometry first (else DINR_ESTATE). */
+dinr_status dinr_set_field_weights(dinr_ctx *ctx, const dinr_field_desc *f, const float *B_dev,
+                                   const float *params_dev, void *stream);
+
+/* Forward projection of n flat pixel indices i = m*N + n (N = n_rows*n_cols):
+ *   fhat_dev[n]  log-domain projection -log(I/I0) (eq:logbeerslaw; BEER or LINEAR combine);
+ *   p_sub_dev    [n*S] per-sub-ray line integrals p_s = (chord_s/N_s) sum_j M(r_j) (eq:estforwmod
+ *                with R7), or NULL;
+ *   I0_dev/Ihat_dev: optional [n] blank intensities and predicted intensities
+ *                Ihat = I0 exp(-fhat) (eq:beerstransavg), both NULL or both set.
+ * n = 0 is legal (no work).  idx_dev is int64. */
+dinr_status dinr_project(dinr_ctx *ctx, const int64_t *idx_dev, int64_t n, float *fhat_dev,
+                         float *p_sub_dev, const float *I0_dev, float *Ihat_dev, void *stream);
+
+/* Local loss and gradient (eq:mainsqdist, eq:localoptfunc P:3261-3297; eq:partiald
+ * P:406-423): L = (1/n) sum_i (y_i - fhat_i)^2 over the n pixels; grad_dev[0..P-1] =
+ * dL/dgamma (D5 layout), grad_dev[P] = L.  accumulate = 0 overwrites, 1 adds.  n = 0 writes
+ * zeros (every rank must still join dinr_allreduce_grads). */
+dinr_status dinr_project_and_grad(dinr_ctx *ctx, const int64_t *idx_dev, int64_t n,
+                                  const float *y_dev, float *grad_dev, int accumulate,
+                                  void *stream);
+
+/* Same as dinr_project_and_grad but with HOST buffers (end-to-end entry point): copies
+ * idx_host[n] and y_host[n] to the device, runs the step on `stream`, optionally averages
+ * the gradient over the communicator (allreduce != 0), and copies grad (P+1 floats) back to
+ * grad_host.  Synchronizes `stream` before returning.  Pinned host memory is fastest. */
+dinr_status dinr_project_and_grad_host(dinr_ctx *ctx, const int64_t *idx_host, int64_t n,
+                                       const float *y_host, float *grad_host, int allreduce,
+                                       void *stream);
+
+/* fp64 ray records of kernel K1 (geometry / ray setup) for n pixels: rec_dev[n*S*9] =
+ * {o.x,o.y,o.z, d.x,d.y,d.z, delta_min, delta_max, chord} per sub-ray, where o is the
+ * rotated source, d = rotated detector point - o, [delta_min, delta_max] the FOV bounds
+ * clamped to [0,1] (eq:solvquaddelta/eq:deltaminmax; miss -> (0,0)) and chord
+ * = |det - src|_2 (delta_max - delta_min) (eq:arclength read as the Euclidean norm, R1). */
+dinr_status dinr_ray_records(dinr_ctx *ctx, const int64_t *idx_dev, int64_t n, double *rec_dev,
+                             void *stream);
+
+/* Data-parallel gradient averaging: 128-byte NCCL unique id (rank 0 creates
+ * it, the caller broadcasts it), communicator init, and an in-place
+ * ncclAllReduce(ncclFloat32, ncclAvg) of count floats on `stream` (gradients and the loss
+ * slot are averaged in the same call, R16). */
+dinr_status dinr_nccl_unique_id(void *out_128_bytes);
+dinr_status dinr_comm_init(dinr_ctx *ctx, const void *unique_id_128_bytes, int rank, int world);
+dinr_status dinr_allreduce_grads(dinr_ctx *ctx, float *grad_dev, int64_t count, void *stream);
+
+/* Synchronizes the device and reports sticky device-side errors (DINR_ERANGE), then clears. */
+dinr_status dinr_get_device_status(dinr_ctx *ctx);
+
+/* Instrumentation.  dinr_set_timing(ctx, 1) brackets every kernel this library launches
+ * with CUDA events on the launching stream; dinr_read_timing() synchronizes and returns, for
+ * kernel class `which` (0 = ray setup, 1 = forward MLP, 2 = loss, 3 = backward MLP,
+ * 4 = dW GEMM, 5 = gradient assembly, 6 = weight pack, 7 = all-reduce), the summed device
+ * milliseconds and the launch count since the last reset (reset != 0 clears after reading).
+ * dinr_launch_count() returns the number of kernels launched by this context so far. */
+dinr_status dinr_set_timing(dinr_ctx *ctx, int enable);
+dinr_status dinr_read_timing(dinr_ctx *ctx, int which, double *ms, int64_t *launches, int reset);
+int64_t dinr_launch_count(const dinr_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DINR_H */

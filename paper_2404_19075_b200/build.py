@@ -1,0 +1,53 @@
+"""Build libdinr.so in-tree with nvcc for sm_100a (B200).
+
+    python -m paper_2404_19075_b200.build [--verbose]
+
+The library is a single translation unit (csrc/api.cu includes the kernel headers).  NCCL is
+resolved at run time with dlopen (csrc/nccl_dl.cuh); only its header is used at build time.
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+SO = os.path.join(HERE, "libdinr.so")
+SRC_DIR = os.path.join(HERE, "csrc")
+INC = os.path.join(os.path.dirname(HERE), "include")
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+
+
+def _sources():
+    out = [os.path.join(INC, "dinr.h")]
+    for f in sorted(os.listdir(SRC_DIR)):
+        if f.endswith((".cu", ".cuh")):
+            out.append(os.path.join(SRC_DIR, f))
+    return out
+
+
+def needs_build() -> bool:
+    if not os.path.exists(SO):
+        return True
+    t = os.path.getmtime(SO)
+    return any(os.path.getmtime(s) > t for s in _sources())
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    if not force and not needs_build():
+        return SO
+    cmd = [
+        NVCC, "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
+        "-Xcompiler", "-fPIC,-O2", "-shared", "-o", SO + ".tmp", os.path.join(SRC_DIR, "api.cu"),
+        "-I", INC, "-ldl",
+    ]
+    if verbose:
+        cmd.insert(1, "-Xptxas=-v")
+    subprocess.check_call(cmd)
+    os.replace(SO + ".tmp", SO)
+    return SO
+
+
+if __name__ == "__main__":
+    build(force=True, verbose="--verbose" in sys.argv)
+    print(SO)

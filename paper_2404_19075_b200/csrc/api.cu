@@ -1,0 +1,792 @@
+// api.cu -- libdinr.so: the C ABI of include/dinr.h.  Host-side validation, scratch
+// management, kernel launches (all stream-ordered on the caller's stream), NCCL plumbing and
+// instrumentation.  Kernels live in the included .cuh files (single translation unit).
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "internal.cuh"
+#include "k_geometry.cuh"
+#include "k_simt.cuh"
+#include "k_small.cuh"
+#include "k_tc_dw.cuh"
+#include "k_tc_mlp.cuh"
+#include "nccl_dl.cuh"
+
+using namespace dinr;
+
+namespace {
+
+thread_local std::string g_static_err;
+
+dinr_status fail(dinr_ctx *c, dinr_status s, const std::string &msg) {
+  if (c) c->err = msg;
+  return s;
+}
+
+#define CUDA_TRY(c, expr)                                                                     \
+  do {                                                                                        \
+    cudaError_t _e = (expr);                                                                  \
+    if (_e != cudaSuccess) return fail((c), DINR_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+  } while (0)
+
+// Kernel-launch bracket: counts the launch and, when timing is on, records CUDA events on
+// the launching stream around it.
+struct Launch {
+  dinr_ctx *c;
+  int cls;
+  cudaStream_t st;
+  cudaEvent_t a = nullptr, b = nullptr;
+  Launch(dinr_ctx *c_, int cls_, cudaStream_t st_) : c(c_), cls(cls_), st(st_) {
+    c->launches++;
+    if (c->timing) {
+      a = take();
+      b = take();
+      cudaEventRecord(a, st);
+    }
+  }
+  cudaEvent_t take() {
+    if (c->event_pool.empty()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      return e;
+    }
+    cudaEvent_t e = c->event_pool.back();
+    c->event_pool.pop_back();
+    return e;
+  }
+  ~Launch() {
+    if (a) {
+      cudaEventRecord(b, st);
+      c->pending.push_back({cls, a, b});
+    }
+  }
+};
+
+bool is_fin(double x) { return std::isfinite(x); }
+
+// Carve a scratch arena into 256-B aligned pieces.
+struct Arena {
+  uint8_t *base;
+  size_t off = 0;
+  explicit Arena(void *b) : base((uint8_t *)b) {}
+  template <class T>
+  T *take(size_t count) {
+    off = (off + 255) & ~size_t(255);
+    T *p = base ? reinterpret_cast<T *>(base + off) : nullptr;
+    off += count * sizeof(T);
+    return p;
+  }
+};
+
+struct Plan {
+  int64_t n, n_rays, nsamp, n_tiles;
+  int nc;
+  int grid_tc;
+  int ksplit, nmb;
+  int ksplit_simt;
+  int nloss;
+  // carved pointers
+  float4 *rec32;
+  float *pchunk, *u, *fhat, *loss_part, *head_part, *dw_part, *db_part, *colsum;
+  uint8_t *hstash, *dstash, *zstash;
+  float *sh, *sz, *sd;
+  int64_t *idx_dev;
+  float *y_dev, *grad_dev;
+};
+
+int loss_blocks_for(int64_t n) { return (int)std::max<int64_t>(1, (n + kLossThreads - 1) / kLossThreads); }
+
+int tc_occupancy(const dinr_ctx *c) {
+  // one CTA per SM for H >= 128 (shared memory); up to 4 for H = 64
+  return c->H == 64 ? 4 : 1;
+}
+
+bool tc_resident(int H, int L) { return (size_t)L * H * H * 2 + (size_t)H * 256 <= 180 * 1024; }
+
+size_t plan_layout(dinr_ctx *c, int64_t n, bool train, bool host_io, Plan &pl, void *base) {
+  Arena ar(base);
+  pl.n = n;
+  pl.n_rays = n * c->S;
+  pl.nsamp = pl.n_rays * c->geom.samples_per_ray;
+  pl.nc = c->geom.samples_per_ray / kChunk;
+  pl.n_tiles = (pl.nsamp + 127) / 128;
+  pl.grid_tc = (int)std::max<int64_t>(1, std::min<int64_t>(pl.n_tiles, (int64_t)c->sm_count * tc_occupancy(c)));
+  pl.nmb = c->H == 256 ? 2 : 1;
+  pl.ksplit = (int)std::max<int64_t>(1, std::min<int64_t>(pl.n_tiles, (c->sm_count + pl.nmb * c->L - 1) / (pl.nmb * c->L)));
+  pl.ksplit_simt = (int)std::max<int64_t>(1, std::min<int64_t>(64, pl.nsamp / 1024));
+  pl.nloss = loss_blocks_for(n);
+  const int H = c->H, L = c->L;
+  pl.rec32 = ar.take<float4>(2 * pl.n_rays + 2);
+  pl.pchunk = ar.take<float>(pl.nsamp / kChunk + 1);
+  pl.u = ar.take<float>(pl.n_rays + 1);
+  pl.fhat = ar.take<float>(n + 1);
+  pl.loss_part = ar.take<float>(pl.nloss + 1);
+  const bool simt = c->field.precision == DINR_FP32_VERIFY;
+  const int ks = simt ? pl.ksplit_simt : pl.ksplit;
+  pl.head_part = ar.take<float>((size_t)std::max(pl.grid_tc, ks) * (H + 1));
+  pl.dw_part = pl.db_part = nullptr;
+  pl.hstash = pl.dstash = pl.zstash = nullptr;
+  pl.sh = pl.sz = pl.sd = pl.colsum = nullptr;
+  if (train) {
+    pl.dw_part = ar.take<float>((size_t)L * pl.nmb * ks * 128 * H);
+    pl.db_part = ar.take<float>((size_t)L * pl.nmb * ks * 128);
+  }
+  if (!simt && train) {
+    pl.hstash = ar.take<uint8_t>((size_t)L * pl.n_tiles * H * 256);
+    pl.dstash = ar.take<uint8_t>((size_t)L * pl.n_tiles * H * 256);
+    pl.zstash = ar.take<uint8_t>((size_t)std::max(1, L - 1) * pl.n_tiles * H * 256);
+  }
+  if (simt) {
+    pl.sh = ar.take<float>((size_t)(L + 1) * pl.nsamp * H);
+    pl.sz = ar.take<float>((size_t)L * pl.nsamp * H);
+    pl.sd = ar.take<float>((size_t)pl.nsamp * H);
+  }
+  pl.idx_dev = nullptr;
+  pl.y_dev = pl.grad_dev = nullptr;
+  if (host_io) {
+    pl.idx_dev = ar.take<int64_t>(n + 1);
+    pl.y_dev = ar.take<float>(n + 1);
+    pl.grad_dev = ar.take<float>(c->P + 1);
+  }
+  return ar.off + 1024;
+}
+
+dinr_status ensure_plan(dinr_ctx *c, int64_t n, bool train, bool host_io, Plan &pl) {
+  size_t need = plan_layout(c, n, train, host_io, pl, nullptr);
+  if (need > c->scratch_cap) {
+    if (c->scratch) cudaFree(c->scratch);
+    c->scratch = nullptr;
+    c->scratch_cap = 0;
+    size_t cap = need + need / 4;
+    if (cudaMalloc(&c->scratch, cap) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(c, DINR_ENOMEM, "scratch allocation of " + std::to_string(cap) + " bytes failed");
+    }
+    c->scratch_cap = cap;
+  }
+  plan_layout(c, n, train, host_io, pl, c->scratch);
+  return DINR_OK;
+}
+
+GeomParams geom_params(const dinr_ctx *c) {
+  const dinr_geometry &g = c->geom;
+  GeomParams gp;
+  gp.beam = g.beam;
+  gp.n_rows = g.n_rows;
+  gp.n_cols = g.n_cols;
+  gp.sub_x = g.sub_x;
+  gp.sub_z = g.sub_z;
+  gp.n_s = g.samples_per_ray;
+  gp.sod = g.sod;
+  gp.odd = g.odd;
+  gp.dx = g.pixel_dx;
+  gp.dz = g.pixel_dz;
+  gp.cx = g.offset_cx;
+  gp.cz = g.offset_cz;
+  gp.r = g.fov_radius;
+  gp.xs0 = g.rot_center_x;
+  gp.zc = 0.5 * (g.z_lo + g.z_hi);
+  gp.zh = 0.5 * (g.z_hi - g.z_lo);
+  gp.tc = 0.5 * (g.t_lo + g.t_hi);
+  gp.th = 0.5 * (g.t_hi - g.t_lo);
+  gp.M = c->M;
+  return gp;
+}
+
+template <class K>
+dinr_status set_smem(dinr_ctx *c, K kernel, size_t bytes) {
+  CUDA_TRY(c, cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  return DINR_OK;
+}
+
+dinr_status launch_rays(dinr_ctx *c, const int64_t *idx, int64_t n, double *rec64, float4 *rec32, cudaStream_t st) {
+  if (n == 0) return DINR_OK;
+  int64_t threads = n * c->S;
+  Launch L_(c, T_RAYS, st);
+  k_ray_setup<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(geom_params(c), c->d_views, idx, n, rec64, rec32,
+                                                                  c->d_flags);
+  CUDA_TRY(c, cudaGetLastError());
+  return DINR_OK;
+}
+
+FieldDev field_dev(const dinr_ctx *c) {
+  FieldDev f;
+  f.C = c->C;
+  f.L = c->L;
+  f.H = c->H;
+  f.mu0 = (float)c->field.mu0;
+  f.B = c->d_B;
+  f.params = c->d_params;
+  f.wpack = c->d_wpack;
+  return f;
+}
+
+template <int H>
+dinr_status launch_tc_mlp(dinr_ctx *c, const Plan &pl, bool train, cudaStream_t st) {
+  TcParams p{};
+  p.rec32 = pl.rec32;
+  p.nsamp = pl.nsamp;
+  p.n_s = c->geom.samples_per_ray;
+  p.L = c->L;
+  p.resident = tc_resident(H, c->L) ? 1 : 0;
+  p.mu0 = (float)c->field.mu0;
+  p.params = c->d_params;
+  p.B = c->d_B;
+  p.wpack = c->d_wpack;
+  p.pchunk = pl.pchunk;
+  p.u = pl.u;
+  p.hstash = pl.hstash;
+  p.dstash = pl.dstash;
+  p.zstash = pl.zstash;
+  p.head_part = pl.head_part;
+  p.n_tiles = pl.n_tiles;
+  size_t smem = TcLayout<H>::smem_bytes(c->L, p.resident != 0);
+  if (train) {
+    dinr_status s = set_smem(c, k_tc_mlp<H, true>, smem);
+    if (s) return s;
+    Launch L_(c, T_BWD, st);
+    k_tc_mlp<H, true><<<pl.grid_tc, 128, smem, st>>>(p);
+  } else {
+    dinr_status s = set_smem(c, k_tc_mlp<H, false>, smem);
+    if (s) return s;
+    Launch L_(c, T_FWD, st);
+    k_tc_mlp<H, false><<<pl.grid_tc, 128, smem, st>>>(p);
+  }
+  CUDA_TRY(c, cudaGetLastError());
+  return DINR_OK;
+}
+
+template <int H>
+dinr_status launch_tc_dw(dinr_ctx *c, const Plan &pl, cudaStream_t st) {
+  DwParams p{};
+  p.hstash = pl.hstash;
+  p.dstash = pl.dstash;
+  p.n_tiles = pl.n_tiles;
+  p.L = c->L;
+  p.ksplit = pl.ksplit;
+  p.nmb = pl.nmb;
+  p.dw_part = pl.dw_part;
+  p.db_part = pl.db_part;
+  size_t smem = DwLayout<H>::smem_bytes();
+  dinr_status s = set_smem(c, k_tc_dw<H>, smem);
+  if (s) return s;
+  Launch L_(c, T_DW, st);
+  k_tc_dw<H><<<dim3(pl.ksplit, pl.nmb, c->L), 128, smem, st>>>(p);
+  CUDA_TRY(c, cudaGetLastError());
+  return DINR_OK;
+}
+
+dinr_status tc_forward(dinr_ctx *c, const Plan &pl, bool train, cudaStream_t st) {
+  switch (c->H) {
+    case 64: return launch_tc_mlp<64>(c, pl, train, st);
+    case 128: return launch_tc_mlp<128>(c, pl, train, st);
+    case 256: return launch_tc_mlp<256>(c, pl, train, st);
+  }
+  return fail(c, DINR_EINVAL, "unsupported width");
+}
+
+dinr_status tc_dw(dinr_ctx *c, const Plan &pl, cudaStream_t st) {
+  switch (c->H) {
+    case 64: return launch_tc_dw<64>(c, pl, st);
+    case 128: return launch_tc_dw<128>(c, pl, st);
+    case 256: return launch_tc_dw<256>(c, pl, st);
+  }
+  return fail(c, DINR_EINVAL, "unsupported width");
+}
+
+// ---------------------------------------------------------------- fp32 SIMT verify path
+dinr_status simt_gemm(dinr_ctx *c, const SgemmArgs &a, int splits, cudaStream_t st, int cls) {
+  dim3 grid((unsigned)((a.N + 63) / 64), (unsigned)((a.M + 63) / 64), (unsigned)splits);
+  Launch L_(c, cls, st);
+  s_gemm<<<grid, 256, 0, st>>>(a);
+  CUDA_TRY(c, cudaGetLastError());
+  return DINR_OK;
+}
+
+dinr_status simt_forward(dinr_ctx *c, const Plan &pl, cudaStream_t st) {
+  const int H = c->H, L = c->L;
+  const int64_t ns = pl.nsamp;
+  {
+    Launch L_(c, T_FWD, st);
+    s_features<<<(unsigned)((ns + 255) / 256), 256, 0, st>>>(pl.rec32, ns, c->geom.samples_per_ray, c->d_B, c->C,
+                                                           pl.sh);
+  }
+  CUDA_TRY(c, cudaGetLastError());
+  const int64_t per = (int64_t)H * H + H;
+  for (int l = 0; l < L; ++l) {
+    SgemmArgs a{};
+    a.A = pl.sh + (size_t)l * ns * H;
+    a.sam = H;
+    a.sak = 1;
+    a.B = c->d_params + l * per;  // B(k=i, n=o) = W[o][i]
+    a.sbk = 1;
+    a.sbn = H;
+    a.M = ns;
+    a.N = H;
+    a.K = H;
+    a.kchunk = H;
+    a.mode = 1;
+    a.ldc = H;
+    a.bias = c->d_params + l * per + (int64_t)H * H;
+    a.Z = pl.sz + (size_t)l * ns * H;
+    a.Hout = pl.sh + (size_t)(l + 1) * ns * H;
+    dinr_status s = simt_gemm(c, a, 1, st, T_FWD);
+    if (s) return s;
+  }
+  {
+    Launch L_(c, T_FWD, st);
+    s_head<<<(unsigned)((ns + 255) / 256), 256, 0, st>>>(pl.sh + (size_t)L * ns * H, ns, H,
+                                                       c->d_params + L * per, (float)c->field.mu0, pl.pchunk);
+  }
+  CUDA_TRY(c, cudaGetLastError());
+  return DINR_OK;
+}
+
+dinr_status simt_backward(dinr_ctx *c, const Plan &pl, cudaStream_t st) {
+  const int H = c->H, L = c->L, ks = pl.ksplit_simt;
+  const int64_t ns = pl.nsamp, per = (int64_t)H * H + H;
+  const int n_s = c->geom.samples_per_ray;
+  const int64_t rows_per = (ns + ks - 1) / ks;
+  const float *wo = c->d_params + L * per;
+  // head partials: sum_rows u h_L and sum u
+  {
+    Launch L_(c, T_BWD, st);
+    s_colsum<<<dim3((unsigned)((H + 1 + 127) / 128), ks), 128, 0, st>>>(pl.sh + (size_t)L * ns * H, ns, H, rows_per,
+                                                                       pl.u, n_s, pl.head_part, H + 1, 128, 1);
+  }
+  // delta_L = u w_o * swish'(z_L)
+  {
+    Launch L_(c, T_BWD, st);
+    s_delta<<<(unsigned)((ns * H + 255) / 256), 256, 0, st>>>(pl.sd, pl.sz + (size_t)(L - 1) * ns * H, ns, H, pl.u,
+                                                            n_s, wo);
+  }
+  for (int l = L - 1; l >= 0; --l) {
+    // dW_l = delta_l^T h_l (split-K partials into dw_part [l][mb][ks][128][H])
+    SgemmArgs a{};
+    a.A = pl.sd;
+    a.sam = 1;
+    a.sak = H;
+    a.B = pl.sh + (size_t)l * ns * H;
+    a.sbk = H;
+    a.sbn = 1;
+    a.M = H;
+    a.N = H;
+    a.K = ns;
+    a.kchunk = rows_per;
+    a.mode = 0;
+    a.C = pl.dw_part + (size_t)l * pl.nmb * ks * 128 * H;
+    a.ldc = H;
+    a.cz = 128 * H;
+    a.cmb = (int64_t)ks * 128 * H;
+    dinr_status s = simt_gemm(c, a, ks, st, T_DW);
+    if (s) return s;
+    {
+      Launch L_(c, T_DW, st);
+      s_colsum<<<dim3((unsigned)((H + 127) / 128), ks), 128, 0, st>>>(
+          pl.sd, ns, H, rows_per, nullptr, n_s, pl.db_part + (size_t)l * pl.nmb * ks * 128, 128, (int64_t)ks * 128, 0);
+    }
+    if (l > 0) {
+      // e_{l-1} = delta_l W_l  (into the z buffer of layer l, which is no longer needed)
+      float *e = pl.sz + (size_t)l * ns * H;
+      SgemmArgs b{};
+      b.A = pl.sd;
+      b.sam = H;
+      b.sak = 1;
+      b.B = c->d_params + l * per;  // B(k=o, n=i) = W[o][i]
+      b.sbk = H;
+      b.sbn = 1;
+      b.M = ns;
+      b.N = H;
+      b.K = H;
+      b.kchunk = H;
+      b.mode = 0;
+      b.C = e;
+      b.ldc = H;
+      b.cz = 0;
+      b.cmb = 128 * H;
+      s = simt_gemm(c, b, 1, st, T_BWD);
+      if (s) return s;
+      {
+        Launch L_(c, T_BWD, st);
+        s_delta<<<(unsigned)((ns * H + 255) / 256), 256, 0, st>>>(e, pl.sz + (size_t)(l - 1) * ns * H, ns, H,
+                                                                nullptr, n_s, nullptr);
+      }
+      CUDA_TRY(c, cudaMemcpyAsync(pl.sd, e, sizeof(float) * ns * H, cudaMemcpyDeviceToDevice, st));
+    }
+  }
+  CUDA_TRY(c, cudaGetLastError());
+  return DINR_OK;
+}
+
+dinr_status run_loss(dinr_ctx *c, const Plan &pl, const float *y, float *fhat, float *p_sub, const float *I0,
+                     float *Ihat, cudaStream_t st) {
+  if (pl.n == 0) return DINR_OK;
+  Launch L_(c, T_LOSS, st);
+  k_loss<<<pl.nloss, kLossThreads, 0, st>>>(pl.rec32, pl.pchunk, c->S, pl.nc, pl.n, y, c->field.combine,
+                                            (float)c->field.mu0, fhat, p_sub, I0, Ihat, pl.u,
+                                            y ? pl.loss_part : nullptr);
+  CUDA_TRY(c, cudaGetLastError());
+  return DINR_OK;
+}
+
+dinr_status step_grad(dinr_ctx *c, const int64_t *idx, int64_t n, const float *y, float *grad, int accumulate,
+                      Plan &pl, cudaStream_t st) {
+  dinr_status s;
+  if (n == 0) {
+    if (!accumulate) CUDA_TRY(c, cudaMemsetAsync(grad, 0, sizeof(float) * (c->P + 1), st));
+    return DINR_OK;
+  }
+  s = launch_rays(c, idx, n, nullptr, pl.rec32, st);
+  if (s) return s;
+  const bool simt = c->field.precision == DINR_FP32_VERIFY;
+  if (simt) {
+    s = simt_forward(c, pl, st);
+  } else {
+    s = tc_forward(c, pl, false, st);
+  }
+  if (s) return s;
+  s = run_loss(c, pl, y, pl.fhat, nullptr, nullptr, nullptr, st);
+  if (s) return s;
+  int nhead, ks;
+  if (simt) {
+    s = simt_backward(c, pl, st);
+    nhead = pl.ksplit_simt;
+    ks = pl.ksplit_simt;
+  } else {
+    s = tc_forward(c, pl, true, st);
+    if (s) return s;
+    s = tc_dw(c, pl, st);
+    nhead = pl.grid_tc;
+    ks = pl.ksplit;
+  }
+  if (s) return s;
+  {
+    Launch L_(c, T_ASM, st);
+    k_assemble<<<(unsigned)((c->P + 1 + 255) / 256), 256, 0, st>>>(c->H, c->L, c->P, pl.nmb, ks, pl.dw_part,
+                                                                   pl.db_part, pl.head_part, nhead, pl.loss_part,
+                                                                   pl.nloss, 1.f / (float)n, accumulate, grad);
+  }
+  CUDA_TRY(c, cudaGetLastError());
+  return DINR_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int64_t dinr_param_count(int32_t n_freq, int32_t n_layers) {
+  int64_t H = 2 * (int64_t)n_freq;
+  return (int64_t)n_layers * (H * H + H) + H + 1;
+}
+
+const char *dinr_status_string(dinr_status s) {
+  switch (s) {
+    case DINR_OK: return "DINR_OK";
+    case DINR_EINVAL: return "DINR_EINVAL";
+    case DINR_ERANGE: return "DINR_ERANGE";
+    case DINR_ENOMEM: return "DINR_ENOMEM";
+    case DINR_ECUDA: return "DINR_ECUDA";
+    case DINR_ENCCL: return "DINR_ENCCL";
+    case DINR_ESTATE: return "DINR_ESTATE";
+    case DINR_EDEVICE: return "DINR_EDEVICE";
+  }
+  return "DINR_UNKNOWN";
+}
+
+dinr_status dinr_create(int device, dinr_ctx **out) {
+  if (!out) return DINR_EINVAL;
+  *out = nullptr;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
+    cudaGetLastError();
+    return DINR_EDEVICE;
+  }
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess || prop.major != 10) return DINR_EDEVICE;
+  dinr_ctx *c = new (std::nothrow) dinr_ctx();
+  if (!c) return DINR_ENOMEM;
+  c->device = device;
+  c->sm_count = prop.multiProcessorCount;
+  if (cudaSetDevice(device) != cudaSuccess || cudaMalloc(&c->d_flags, 16) != cudaSuccess ||
+      cudaMemset(c->d_flags, 0, 16) != cudaSuccess) {
+    delete c;
+    return DINR_ECUDA;
+  }
+  *out = c;
+  return DINR_OK;
+}
+
+dinr_status dinr_destroy(dinr_ctx *c) {
+  if (!c) return DINR_EINVAL;
+  cudaSetDevice(c->device);
+  for (auto &p : c->pending) {
+    cudaEventDestroy(p.a);
+    cudaEventDestroy(p.b);
+  }
+  for (auto e : c->event_pool) cudaEventDestroy(e);
+  if (c->comm) nccl().CommDestroy((ncclComm_t)c->comm);
+  cudaFree(c->d_views);
+  cudaFree(c->d_B);
+  cudaFree(c->d_params);
+  cudaFree(c->d_wpack);
+  cudaFree(c->scratch);
+  cudaFree(c->d_flags);
+  delete c;
+  return DINR_OK;
+}
+
+const char *dinr_last_error(const dinr_ctx *c) { return c ? c->err.c_str() : "null context"; }
+
+dinr_status dinr_set_geometry(dinr_ctx *c, const dinr_geometry *g, const double *theta, const double *t, int64_t M) {
+  if (!c || !g || !theta || !t) return c ? fail(c, DINR_EINVAL, "null argument") : DINR_EINVAL;
+  if (g->beam < 0 || g->beam > 2) return fail(c, DINR_EINVAL, "beam must be 0 (parallel), 1 (fan) or 2 (cone)");
+  if (g->n_rows < 1 || g->n_cols < 1) return fail(c, DINR_EINVAL, "n_rows, n_cols must be >= 1");
+  if (g->sub_x < 1 || g->sub_z < 1 || g->sub_x * g->sub_z > kMaxS)
+    return fail(c, DINR_EINVAL, "sub_x, sub_z must be >= 1 with sub_x*sub_z <= 16");
+  if (g->samples_per_ray < 32 || g->samples_per_ray % 32)
+    return fail(c, DINR_EINVAL, "samples_per_ray must be a positive multiple of 32");
+  const double v[] = {g->sod, g->odd, g->pixel_dx, g->pixel_dz, g->offset_cx, g->offset_cz, g->fov_radius,
+                      g->rot_center_x, g->z_lo, g->z_hi, g->t_lo, g->t_hi};
+  for (double x : v)
+    if (!is_fin(x)) return fail(c, DINR_EINVAL, "geometry values must be finite");
+  if (!(g->sod > 0) || !(g->odd >= 0) || !(g->pixel_dx > 0) || !(g->pixel_dz > 0) || !(g->fov_radius > 0))
+    return fail(c, DINR_EINVAL, "need sod > 0, odd >= 0, pixel pitches > 0, fov_radius > 0 (S:24-27)");
+  if (!(g->fov_radius < g->sod)) return fail(c, DINR_EINVAL, "fov_radius must be < sod (source outside the FOV)");
+  if (!(g->z_hi >= g->z_lo) || !(g->t_hi >= g->t_lo)) return fail(c, DINR_EINVAL, "normalization ranges inverted");
+  if (M < 1) return fail(c, DINR_EINVAL, "M must be >= 1");
+  for (int64_t k = 0; k < M; ++k) {
+    if (!is_fin(theta[k]) || !is_fin(t[k])) return fail(c, DINR_EINVAL, "non-finite view angle or time");
+    if (k > 0 && t[k] < t[k - 1]) return fail(c, DINR_EINVAL, "view times must be non-decreasing");
+  }
+  std::vector<double> tab((size_t)M * 3);
+  for (int64_t k = 0; k < M; ++k) {  // host libm, same as the oracle (O1)
+    tab[3 * k] = std::cos(theta[k]);
+    tab[3 * k + 1] = std::sin(theta[k]);
+    tab[3 * k + 2] = t[k];
+  }
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  double *dv = nullptr;
+  CUDA_TRY(c, cudaMalloc(&dv, sizeof(double) * tab.size()));
+  if (cudaMemcpy(dv, tab.data(), sizeof(double) * tab.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
+    cudaFree(dv);
+    return fail(c, DINR_ECUDA, "view table upload failed");
+  }
+  cudaFree(c->d_views);
+  c->d_views = dv;
+  c->geom = *g;
+  c->M = M;
+  c->S = g->sub_x * g->sub_z;
+  c->have_geom = true;
+  return DINR_OK;
+}
+
+dinr_status dinr_set_field_weights(dinr_ctx *c, const dinr_field_desc *f, const float *B_dev, const float *params_dev,
+                                   void *stream) {
+  if (!c || !f || !B_dev || !params_dev) return c ? fail(c, DINR_EINVAL, "null argument") : DINR_EINVAL;
+  if (!c->have_geom) return fail(c, DINR_ESTATE, "dinr_set_geometry must be called first");
+  if (f->n_freq < 1 || f->width != 2 * f->n_freq || f->n_layers < 1 || f->n_layers > 64)
+    return fail(c, DINR_EINVAL, "need n_freq >= 1, width == 2*n_freq, 1 <= n_layers <= 64");
+  if (!(f->mu0 > 0) || !is_fin(f->mu0)) return fail(c, DINR_EINVAL, "mu0 must be > 0");
+  if (f->combine != DINR_BEER && f->combine != DINR_LINEAR) return fail(c, DINR_EINVAL, "bad combine");
+  if (f->precision == DINR_BF16) {
+    if (f->width != 64 && f->width != 128 && f->width != 256)
+      return fail(c, DINR_EINVAL, "BF16 path supports width 64, 128 or 256");
+  } else if (f->precision == DINR_FP32_VERIFY) {
+    if (f->width > kMaxH || f->width % 2) return fail(c, DINR_EINVAL, "FP32_VERIFY supports width <= 256");
+  } else {
+    return fail(c, DINR_EINVAL, "bad precision");
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  const int H = f->width, L = f->n_layers;
+  const int64_t P = dinr_param_count(f->n_freq, f->n_layers);
+  size_t pbytes = sizeof(float) * (P + 4);
+  if (pbytes > c->params_cap) {
+    cudaFree(c->d_params);
+    c->d_params = nullptr;
+    CUDA_TRY(c, cudaMalloc(&c->d_params, pbytes));
+    c->params_cap = pbytes;
+  }
+  size_t wbytes = (size_t)L * H * H * 2;
+  if (wbytes > c->wpack_cap) {
+    cudaFree(c->d_wpack);
+    c->d_wpack = nullptr;
+    CUDA_TRY(c, cudaMalloc(&c->d_wpack, wbytes));
+    c->wpack_cap = wbytes;
+  }
+  if (!c->d_B || f->n_freq > c->C) {
+    cudaFree(c->d_B);
+    c->d_B = nullptr;
+    CUDA_TRY(c, cudaMalloc(&c->d_B, sizeof(float) * 4 * std::max(f->n_freq, kMaxH / 2)));
+  }
+  CUDA_TRY(c, cudaMemcpyAsync(c->d_B, B_dev, sizeof(float) * 4 * f->n_freq, cudaMemcpyDeviceToDevice, st));
+  CUDA_TRY(c, cudaMemcpyAsync(c->d_params, params_dev, sizeof(float) * P, cudaMemcpyDeviceToDevice, st));
+  c->field = *f;
+  c->C = f->n_freq;
+  c->L = L;
+  c->H = H;
+  c->P = P;
+  if (f->precision == DINR_BF16) {
+    Launch L_(c, T_PACK, st);
+    int64_t tot = (int64_t)L * H * H;
+    k_pack_weights<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(c->d_params, H, L, c->d_wpack);
+  }
+  CUDA_TRY(c, cudaGetLastError());
+  c->have_field = true;
+  return DINR_OK;
+}
+
+dinr_status dinr_ray_records(dinr_ctx *c, const int64_t *idx, int64_t n, double *rec, void *stream) {
+  if (!c) return DINR_EINVAL;
+  if (!c->have_geom) return fail(c, DINR_ESTATE, "dinr_set_geometry must be called first");
+  if (n < 0 || (n > 0 && (!idx || !rec))) return fail(c, DINR_EINVAL, "bad arguments");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  return launch_rays(c, idx, n, rec, nullptr, (cudaStream_t)stream);
+}
+
+dinr_status dinr_project(dinr_ctx *c, const int64_t *idx, int64_t n, float *fhat, float *p_sub, const float *I0,
+                         float *Ihat, void *stream) {
+  if (!c) return DINR_EINVAL;
+  if (!c->have_geom || !c->have_field) return fail(c, DINR_ESTATE, "geometry and field weights must be set first");
+  if (n < 0 || (n > 0 && (!idx || !fhat)) || ((I0 == nullptr) != (Ihat == nullptr)))
+    return fail(c, DINR_EINVAL, "bad arguments");
+  if (n == 0) return DINR_OK;
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  Plan pl;
+  dinr_status s = ensure_plan(c, n, false, false, pl);
+  if (s) return s;
+  s = launch_rays(c, idx, n, nullptr, pl.rec32, st);
+  if (s) return s;
+  s = c->field.precision == DINR_FP32_VERIFY ? simt_forward(c, pl, st) : tc_forward(c, pl, false, st);
+  if (s) return s;
+  return run_loss(c, pl, nullptr, fhat, p_sub, I0, Ihat, st);
+}
+
+dinr_status dinr_project_and_grad(dinr_ctx *c, const int64_t *idx, int64_t n, const float *y, float *grad,
+                                  int accumulate, void *stream) {
+  if (!c) return DINR_EINVAL;
+  if (!c->have_geom || !c->have_field) return fail(c, DINR_ESTATE, "geometry and field weights must be set first");
+  if (n < 0 || !grad || (n > 0 && (!idx || !y))) return fail(c, DINR_EINVAL, "bad arguments");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  Plan pl;
+  dinr_status s = ensure_plan(c, n, true, false, pl);
+  if (s) return s;
+  return step_grad(c, idx, n, y, grad, accumulate, pl, (cudaStream_t)stream);
+}
+
+dinr_status dinr_project_and_grad_host(dinr_ctx *c, const int64_t *idx_host, int64_t n, const float *y_host,
+                                       float *grad_host, int allreduce, void *stream) {
+  if (!c) return DINR_EINVAL;
+  if (!c->have_geom || !c->have_field) return fail(c, DINR_ESTATE, "geometry and field weights must be set first");
+  if (n < 0 || !grad_host || (n > 0 && (!idx_host || !y_host))) return fail(c, DINR_EINVAL, "bad arguments");
+  if (allreduce && !c->comm && c->world > 1) return fail(c, DINR_ESTATE, "communicator not initialized");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  Plan pl;
+  dinr_status s = ensure_plan(c, n, true, true, pl);
+  if (s) return s;
+  if (n > 0) {
+    CUDA_TRY(c, cudaMemcpyAsync(pl.idx_dev, idx_host, sizeof(int64_t) * n, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(c, cudaMemcpyAsync(pl.y_dev, y_host, sizeof(float) * n, cudaMemcpyHostToDevice, st));
+  }
+  s = step_grad(c, pl.idx_dev, n, pl.y_dev, pl.grad_dev, 0, pl, st);
+  if (s) return s;
+  if (allreduce && c->comm) {
+    s = dinr_allreduce_grads(c, pl.grad_dev, c->P + 1, stream);
+    if (s) return s;
+  }
+  CUDA_TRY(c, cudaMemcpyAsync(grad_host, pl.grad_dev, sizeof(float) * (c->P + 1), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(c, cudaStreamSynchronize(st));
+  return DINR_OK;
+}
+
+dinr_status dinr_nccl_unique_id(void *out) {
+  if (!out) return DINR_EINVAL;
+  ncclUniqueId id;
+  if (!nccl().ok || nccl().GetUniqueId(&id) != ncclSuccess) return DINR_ENCCL;
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId must be 128 bytes");
+  std::memcpy(out, &id, sizeof(id));
+  return DINR_OK;
+}
+
+dinr_status dinr_comm_init(dinr_ctx *c, const void *uid, int rank, int world) {
+  if (!c || !uid || world < 1 || rank < 0 || rank >= world) return c ? fail(c, DINR_EINVAL, "bad rank/world") : DINR_EINVAL;
+  if (!nccl().ok) return fail(c, DINR_ENCCL, nccl().err);
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  if (c->comm) {
+    nccl().CommDestroy((ncclComm_t)c->comm);
+    c->comm = nullptr;
+  }
+  ncclUniqueId id;
+  std::memcpy(&id, uid, sizeof(id));
+  ncclComm_t comm;
+  ncclResult_t r = nccl().CommInitRank(&comm, world, id, rank);
+  if (r != ncclSuccess) return fail(c, DINR_ENCCL, std::string("ncclCommInitRank: ") + nccl().GetErrorString(r));
+  c->comm = comm;
+  c->rank = rank;
+  c->world = world;
+  return DINR_OK;
+}
+
+dinr_status dinr_allreduce_grads(dinr_ctx *c, float *grad, int64_t count, void *stream) {
+  if (!c || !grad || count < 0) return c ? fail(c, DINR_EINVAL, "bad arguments") : DINR_EINVAL;
+  if (!c->comm) return fail(c, DINR_ESTATE, "dinr_comm_init must be called first");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  Launch L_(c, T_AR, st);
+  ncclResult_t r = nccl().AllReduce(grad, grad, (size_t)count, ncclFloat32, ncclAvg, (ncclComm_t)c->comm, st);
+  if (r != ncclSuccess) return fail(c, DINR_ENCCL, std::string("ncclAllReduce: ") + nccl().GetErrorString(r));
+  return DINR_OK;
+}
+
+dinr_status dinr_get_device_status(dinr_ctx *c) {
+  if (!c) return DINR_EINVAL;
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  CUDA_TRY(c, cudaDeviceSynchronize());
+  int flags = 0;
+  CUDA_TRY(c, cudaMemcpy(&flags, c->d_flags, sizeof(int), cudaMemcpyDeviceToHost));
+  CUDA_TRY(c, cudaMemset(c->d_flags, 0, sizeof(int)));
+  if (flags & 1) return fail(c, DINR_ERANGE, "a pixel index was out of range (>= M*N); it contributed 0");
+  return DINR_OK;
+}
+
+dinr_status dinr_set_timing(dinr_ctx *c, int enable) {
+  if (!c) return DINR_EINVAL;
+  c->timing = enable != 0;
+  return DINR_OK;
+}
+
+dinr_status dinr_read_timing(dinr_ctx *c, int which, double *ms, int64_t *launches, int reset) {
+  if (!c || which < 0 || which >= T_N) return c ? fail(c, DINR_EINVAL, "bad timer class") : DINR_EINVAL;
+  for (auto &p : c->pending) {
+    CUDA_TRY(c, cudaEventSynchronize(p.b));
+    float e = 0.f;
+    CUDA_TRY(c, cudaEventElapsedTime(&e, p.a, p.b));
+    c->acc_ms[p.cls] += e;
+    c->acc_n[p.cls] += 1;
+    c->event_pool.push_back(p.a);
+    c->event_pool.push_back(p.b);
+  }
+  c->pending.clear();
+  if (ms) *ms = c->acc_ms[which];
+  if (launches) *launches = c->acc_n[which];
+  if (reset) {
+    c->acc_ms[which] = 0;
+    c->acc_n[which] = 0;
+  }
+  return DINR_OK;
+}
+
+int64_t dinr_launch_count(const dinr_ctx *c) { return c ? c->launches : 0; }
+
+}  // extern "C"

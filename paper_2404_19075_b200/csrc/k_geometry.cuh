@@ -1,0 +1,119 @@
+// k_geometry.cuh -- K1 ray setup (north_star subsystem (1)).
+//
+// One thread per sub-ray.  fp64 with explicitly rounded intrinsics (__dadd_rn, __dmul_rn,
+// __ddiv_rn, __dsqrt_rn) so no FMA contraction occurs and the operation order is the
+// one written in DESIGN.md "Ray geometry" (the oracle writes the same formulas in plain C
+// compiled with -ffp-contract=off; cos/sin come from the host libm via the view table):
+//   a1 decode    i = m N + n, row = n / n_cols, col = n % n_cols        (R13)
+//   a3 endpoints x_d = -C_x + (col + (u+1/2)/D_x) dx, y_d = odd,
+//                z_d = -C_z + (row + (v+1/2)/D_z) dz
+//                source cone (0,-sod,0) / fan (0,-sod,z_d) / parallel (x_d,-sod,z_d)
+//                                                                        (R9, R10)
+//   a4 bounds    a = ex^2+ey^2, b = 2(px ex + y_s ey), c = (px^2 + y_s^2) - r^2,
+//                disc = b^2 - 4ac, roots (-b -+ sqrt(disc))/(2a) clamped to [0,1]
+//                                                                        (R21)
+//                arc length s = sqrt(a + ez^2) (P:155-172 read as Euclidean, R1),
+//                chord = s (delta_max - delta_min)
+//   a2 rotation  x' = (x c - y s) + (x_s0 - x_s0 c), y' = (x s + y c) - x_s0 s
+#pragma once
+#include "internal.cuh"
+
+namespace dinr {
+
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+
+__device__ __forceinline__ void rot_cs(double x, double y, double c, double s, double xs0, double &xo,
+                                       double &yo) {
+  xo = dadd(dsub(dmul(x, c), dmul(y, s)), dsub(xs0, dmul(xs0, c)));
+  yo = dsub(dadd(dmul(x, s), dmul(y, c)), dmul(xs0, s));
+}
+
+__global__ void k_ray_setup(GeomParams gp, const double *__restrict__ views, const int64_t *__restrict__ idx,
+                            int64_t n, double *__restrict__ rec64, float4 *__restrict__ rec32,
+                            int *__restrict__ flags) {
+  const int S = gp.sub_x * gp.sub_z;
+  int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= n * S) return;
+  int64_t p = gid / S;
+  int s = (int)(gid - p * S);
+  int u = s % gp.sub_x, v = s / gp.sub_x;
+  int64_t i = idx[p];
+  int64_t N = (int64_t)gp.n_rows * gp.n_cols;
+  if (i < 0 || i >= gp.M * N) {
+    atomicOr(flags, 1);
+    if (rec64)
+      for (int q = 0; q < 9; ++q) rec64[gid * 9 + q] = 0.0;
+    if (rec32) {
+      rec32[2 * gid] = make_float4(0.f, 0.f, 0.f, 0.f);
+      rec32[2 * gid + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    return;
+  }
+  int64_t k = i / N, nn = i % N;
+  int64_t row = nn / gp.n_cols, col = nn % gp.n_cols;
+  double ck = views[3 * k], sk = views[3 * k + 1], tk = views[3 * k + 2];
+
+  double xd = dadd(-gp.cx, dmul(dadd((double)col, __ddiv_rn(dadd((double)u, 0.5), (double)gp.sub_x)), gp.dx));
+  double yd = gp.odd;
+  double zd = dadd(-gp.cz, dmul(dadd((double)row, __ddiv_rn(dadd((double)v, 0.5), (double)gp.sub_z)), gp.dz));
+  double xs, ys = -gp.sod, zs;
+  if (gp.beam == DINR_CONE) {
+    xs = 0.0;
+    zs = 0.0;
+  } else if (gp.beam == DINR_FAN) {
+    xs = 0.0;
+    zs = zd;
+  } else {
+    xs = xd;
+    zs = zd;
+  }
+  double ex = dsub(xd, xs), ey = dsub(yd, ys), px = dsub(xs, gp.xs0);
+  double a = dadd(dmul(ex, ex), dmul(ey, ey));
+  double b = dmul(2.0, dadd(dmul(px, ex), dmul(ys, ey)));
+  double c = dsub(dadd(dmul(px, px), dmul(ys, ys)), dmul(gp.r, gp.r));
+  double disc = dsub(dmul(b, b), dmul(dmul(4.0, a), c));
+  double dmin = 0.0, dmax = 0.0;
+  if (!(disc < 0.0)) {
+    double q = __dsqrt_rn(disc);
+    double lo = __ddiv_rn(dsub(-b, q), dmul(2.0, a));
+    double hi = __ddiv_rn(dadd(-b, q), dmul(2.0, a));
+    dmin = fmin(fmax(lo, 0.0), 1.0);
+    dmax = fmin(fmax(hi, 0.0), 1.0);
+  }
+  double ez = dsub(zd, zs);
+  double sarc = __dsqrt_rn(dadd(a, dmul(ez, ez)));
+  double chord = dmul(sarc, dsub(dmax, dmin));
+  double xsk, ysk, xdk, ydk;
+  rot_cs(xs, ys, ck, sk, gp.xs0, xsk, ysk);
+  rot_cs(xd, yd, ck, sk, gp.xs0, xdk, ydk);
+  double ox = xsk, oy = ysk, oz = zs;
+  double dx = dsub(xdk, xsk), dy = dsub(ydk, ysk), dz = ez;
+  if (rec64) {
+    double *r = rec64 + gid * 9;
+    r[0] = ox;
+    r[1] = oy;
+    r[2] = oz;
+    r[3] = dx;
+    r[4] = dy;
+    r[5] = dz;
+    r[6] = dmin;
+    r[7] = dmax;
+    r[8] = chord;
+  }
+  if (rec32) {
+    // Normalized entry point and per-sample step (R11); weight chord/N_s (R7).
+    double ir = 1.0 / gp.r;
+    double izh = gp.zh > 0.0 ? 1.0 / gp.zh : 0.0;
+    double ex0 = ox + dmin * dx, ey0 = oy + dmin * dy, ez0 = oz + dmin * dz;
+    double step = (dmax - dmin) / (double)gp.n_s;
+    float tb = gp.th > 0.0 ? (float)((tk - gp.tc) / gp.th) : 0.f;
+    bool hit = chord > 0.0;
+    rec32[2 * gid] = make_float4((float)((ex0 - gp.xs0) * ir), (float)(ey0 * ir), (float)((ez0 - gp.zc) * izh), tb);
+    rec32[2 * gid + 1] = make_float4((float)(step * dx * ir), (float)(step * dy * ir), (float)(step * dz * izh),
+                                     hit ? (float)(chord / (double)gp.n_s) : 0.f);
+  }
+}
+
+}  // namespace dinr

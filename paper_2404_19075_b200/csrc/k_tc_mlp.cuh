@@ -1,0 +1,380 @@
+// k_tc_mlp.cuh -- K2 (fused sample -> GRFF -> L x (tcgen05 GEMM + bias + Swish) -> head ->
+// ray-chunk sum) and K3 (same forward recomputed, then the backward dX chain on the tensor
+// cores), north_star subsystems (2) and (3).
+//
+// Tile = 128 consecutive samples (rows) = 128 TMEM lanes; one CTA of 128 threads, thread r
+// owns row r (its sample) in every epilogue; thread 0 issues the tcgen05.mma and the bulk
+// (TMA-engine) copies.  Per layer l the accumulator D[128 x H] (fp32, TMEM) is
+//   forward : D = A(h_l, K-major SW128 smem) . W_l^T   (B = W_l image, K-major)
+//   backward: D = A(delta_l)                  . W_l     (B = same W_l image, MN-major)
+// Weights live in shared memory for the whole kernel when L*H*H*2 fits (H <= 128), else they
+// are streamed one layer at a time with a prefetch issued as soon as the previous MMA retires.
+// K3 writes, per tile, the bf16 images of h_l (layer inputs) and delta_l with bulk
+// shared->global copies (operands of the dW GEMM, k_tc_dw.cuh), keeps z_l in an fp16
+// coalesced stash for swish', and reduces the head gradients (dL/dw_o = sum u h_L,
+// dL/db_o = sum u) with a warp transpose-reduction into registers.
+#pragma once
+#include "internal.cuh"
+#include "ptx_sm100.cuh"
+
+namespace dinr {
+
+struct TcParams {
+  const float4 *rec32;
+  int64_t nsamp;
+  int n_s;
+  int L;
+  int resident;
+  float mu0;
+  const float *params;
+  const float *B;
+  const uint16_t *wpack;
+  float *pchunk;   // forward: [nsamp/32] sums of M over 32-sample chunks
+  // training
+  const float *u;  // [n_rays] upstream for the raw head output (K4)
+  uint8_t *hstash, *dstash, *zstash;
+  float *head_part;  // [gridDim.x][H+1]
+  int64_t n_tiles;
+};
+
+template <int H>
+struct TcLayout {
+  static constexpr uint32_t A_BYTES = H * 256u;        // 128 rows x H bf16
+  static constexpr uint32_t W_LAYER = H * H * 2u;
+  static size_t smem_bytes(int L, bool resident) {
+    size_t w = resident ? (size_t)L * W_LAYER : W_LAYER;
+    return 1024 + A_BYTES + w + (size_t)L * H * 4 + H * 4 + 16 + (H / 2) * 16 + 64;
+  }
+};
+
+__device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
+
+__device__ __forceinline__ float swish_f(float z) { return z * (0.5f + 0.5f * tanh_approx(0.5f * z)); }
+__device__ __forceinline__ float dswish_f(float z) {
+  float s = 0.5f + 0.5f * tanh_approx(0.5f * z);
+  return s * (1.f + z * (1.f - s));
+}
+
+template <int H, bool TRAIN>
+__global__ void __launch_bounds__(128, 1) k_tc_mlp(TcParams p) {
+  constexpr int C = H / 2;
+  constexpr uint32_t A_BYTES = TcLayout<H>::A_BYTES;
+  constexpr uint32_t W_LAYER = TcLayout<H>::W_LAYER;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int L = p.L;
+  const bool resident = p.resident != 0;
+  uint8_t *sA = smem;
+  uint8_t *sW = smem + A_BYTES;
+  float *sBias = reinterpret_cast<float *>(sW + (resident ? (size_t)L * W_LAYER : (size_t)W_LAYER));
+  float *sWo = sBias + L * H;
+  float *sB = sWo + H + 4;
+  uint64_t *bars = reinterpret_cast<uint64_t *>(sB + C * 4);
+  uint64_t *mma_bar = bars, *w_bar = bars + 1;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (warp == 0) {
+    tmem_alloc(tmem_slot, H);
+    tmem_relinquish();
+  }
+  if (tid == 0) {
+    mbar_init(mma_bar, 1);
+    mbar_init(w_bar, 1);
+    fence_mbar_init();
+  }
+  const int64_t per = (int64_t)H * H + H;
+  for (int i = tid; i < L * H; i += 128) sBias[i] = p.params[(i / H) * per + (int64_t)H * H + (i % H)];
+  for (int i = tid; i <= H; i += 128) sWo[i] = p.params[(int64_t)L * per + i];  // w_o, then b_o
+  for (int i = tid; i < C * 4; i += 128) sB[i] = p.B[i];
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t a_base = smem_u32(sA), w_base = smem_u32(sW);
+  const uint32_t tmem_row = tmem + ((uint32_t)(warp * 32) << 16);
+  const int n_tiles = (int)((p.nsamp + 127) / 128);
+
+  // Weight schedule (thread 0): the layer whose image sits in sW, and a pending load.
+  int w_cur = -1;
+  uint32_t w_phase = 0;
+  bool w_pending = false;
+  auto w_issue = [&](int layer) {  // only when no MMA is reading sW
+    uint32_t bytes = resident ? (uint32_t)L * W_LAYER : W_LAYER;
+    const uint8_t *src = reinterpret_cast<const uint8_t *>(p.wpack) + (resident ? 0 : (size_t)layer * W_LAYER);
+    mbar_arrive_expect_tx(w_bar, bytes);
+    for (uint32_t off = 0; off < bytes; off += 32768u)
+      bulk_g2s(sW + off, src + off, min(32768u, bytes - off), w_bar);
+    w_pending = true;
+    w_cur = resident ? -2 : layer;
+  };
+  auto w_ready = [&](int layer) -> uint32_t {
+    if (w_pending) {
+      mbar_wait(w_bar, w_phase);
+      w_phase ^= 1;
+      w_pending = false;
+    }
+    return resident ? w_base + (uint32_t)layer * W_LAYER : w_base;
+  };
+  if (tid == 0 && (int)blockIdx.x < n_tiles) w_issue(0);
+
+  uint32_t mma_phase = 0;
+  float head_acc[H / 32];
+#pragma unroll
+  for (int i = 0; i < H / 32; ++i) head_acc[i] = 0.f;
+  float bo_acc = 0.f;
+  const uint32_t idesc_f = idesc_bf16(128, H, 0, 0);
+  const uint32_t idesc_b = idesc_bf16(128, H, 0, 1);
+
+  for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    const bool more_tiles = tile + (int)gridDim.x < n_tiles;
+    const int row = tid;
+    const int64_t g = (int64_t)tile * 128 + row;
+    const bool valid = g < p.nsamp;
+    float u_row = 0.f;
+    if (TRAIN) {  // the previous tile's last bulk store must be done reading sA
+      if (tid == 0) bulk_wait_read_all();
+      __syncthreads();
+    }
+    // ---------------------------------------------------------------- a5/a6 features
+    {
+      float rb0 = 0.f, rb1 = 0.f, rb2 = 0.f, rb3 = 0.f;
+      if (valid) {
+        int64_t ray = g / p.n_s;
+        float jj = (float)(g - ray * p.n_s) + 0.5f;
+        float4 ra = p.rec32[2 * ray], rbv = p.rec32[2 * ray + 1];
+        rb0 = ra.w;                 // t
+        rb1 = ra.z + jj * rbv.z;    // z
+        rb2 = ra.y + jj * rbv.y;    // y
+        rb3 = ra.x + jj * rbv.x;    // x
+        if (TRAIN) u_row = p.u[ray];
+      }
+#pragma unroll 1
+      for (int c0 = 0; c0 < C; c0 += 8) {
+        uint32_t pc[4], ps[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          float cs[2], sn[2];
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const float *bb = sB + 4 * (c0 + 2 * q + e);
+            float phi = bb[0] * rb0 + bb[1] * rb1 + bb[2] * rb2 + bb[3] * rb3;
+            float fr = phi - rintf(phi);  // range reduction to [-1/2, 1/2]
+            __sincosf(6.283185307179586f * fr, &sn[e], &cs[e]);
+          }
+          pc[q] = pack_bf16x2(cs[0], cs[1]);
+          ps[q] = pack_bf16x2(sn[0], sn[1]);
+        }
+        st_shared_v4(a_base + sw128_offset(row, c0, 128), pc[0], pc[1], pc[2], pc[3]);
+        st_shared_v4(a_base + sw128_offset(row, C + c0, 128), ps[0], ps[1], ps[2], ps[3]);
+      }
+    }
+    fence_proxy_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    if (TRAIN && tid == 0) {
+      bulk_s2g(p.hstash + ((size_t)0 * p.n_tiles + tile) * A_BYTES, sA, A_BYTES);
+      bulk_commit();
+    }
+    // ---------------------------------------------------------------- a7/a8 forward
+    float mu_acc = 0.f;
+    for (int l = 0; l < L; ++l) {
+      if (tid == 0) {
+        uint32_t wl = w_ready(l);
+        tc_fence_after();
+#pragma unroll 4
+        for (int kk = 0; kk < H / 16; ++kk) {
+          uint64_t ad = sdesc_sw128(a_base + (kk >> 2) * (128 * 128) + (kk & 3) * 32, 16, 1024);
+          uint64_t bd = sdesc_sw128(wl + (kk >> 2) * (H * 128) + (kk & 3) * 32, 16, 1024);
+          umma_bf16(tmem, ad, bd, idesc_f, kk > 0 ? 1u : 0u);
+        }
+        umma_commit(mma_bar);
+      }
+      mbar_wait(mma_bar, mma_phase);
+      mma_phase ^= 1;
+      tc_fence_after();
+      if (tid == 0) {
+        // prefetch the next weight image (streaming mode) now that sW is free
+        if (!resident) {
+          int nxt;
+          bool has_next = true;
+          if (!TRAIN) {
+            nxt = (l + 1) % L;
+            has_next = (l + 1 < L) || more_tiles;
+          } else {
+            nxt = (l + 1 < L) ? l + 1 : (L >= 2 ? L - 1 : 0);
+            has_next = (l + 1 < L) || L >= 2 || more_tiles;
+          }
+          if (has_next && nxt != w_cur) w_issue(nxt);
+        }
+        if (TRAIN) bulk_wait_read_all();
+      }
+      if (TRAIN) __syncthreads();
+      const bool last = (l == L - 1);
+#pragma unroll 1
+      for (int cb = 0; cb < H / 32; ++cb) {
+        uint32_t v[32];
+        tmem_ld32(tmem_row + cb * 32, v);
+        tmem_wait_ld();
+        float z[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) z[i] = __uint_as_float(v[i]) + sBias[l * H + cb * 32 + i];
+        if (!last) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            uint32_t w4[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) w4[e] = pack_bf16x2(swish_f(z[8 * q + 2 * e]), swish_f(z[8 * q + 2 * e + 1]));
+            st_shared_v4(a_base + sw128_offset(row, cb * 32 + 8 * q, 128), w4[0], w4[1], w4[2], w4[3]);
+            if (TRAIN) {
+              uint32_t h4[4];
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                __half2 hh = __floats2half2_rn(z[8 * q + 2 * e], z[8 * q + 2 * e + 1]);
+                h4[e] = *reinterpret_cast<uint32_t *>(&hh);
+              }
+              uint4 *dst = reinterpret_cast<uint4 *>(p.zstash) +
+                           ((((size_t)l * p.n_tiles + tile) * (H / 8) + (cb * 4 + q)) * 128 + row);
+              *dst = make_uint4(h4[0], h4[1], h4[2], h4[3]);
+            }
+          }
+        } else if (!TRAIN) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) mu_acc += sWo[cb * 32 + i] * swish_f(z[i]);
+        } else {
+          // head gradients (transpose-reduce u*h_L over the warp's 32 rows) and delta_L
+          float x[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) x[i] = u_row * swish_f(z[i]);
+#pragma unroll
+          for (int o = 16; o >= 1; o >>= 1) {
+            const bool upper = (lane & o) != 0;
+#pragma unroll
+            for (int i = 0; i < o; ++i) {
+              float send = upper ? x[i] : x[i + o];
+              float keep = upper ? x[i + o] : x[i];
+              x[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+            }
+          }
+          head_acc[cb] += x[0];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            uint32_t w4[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              int i0 = 8 * q + 2 * e;
+              float d0 = u_row * sWo[cb * 32 + i0] * dswish_f(z[i0]);
+              float d1 = u_row * sWo[cb * 32 + i0 + 1] * dswish_f(z[i0 + 1]);
+              w4[e] = pack_bf16x2(d0, d1);
+            }
+            st_shared_v4(a_base + sw128_offset(row, cb * 32 + 8 * q, 128), w4[0], w4[1], w4[2], w4[3]);
+          }
+        }
+      }
+      if (!last || TRAIN) fence_proxy_async_smem();
+      tc_fence_before();
+      __syncthreads();
+      if (TRAIN && tid == 0) {
+        uint8_t *dst = last ? p.dstash + ((size_t)(L - 1) * p.n_tiles + tile) * A_BYTES
+                            : p.hstash + ((size_t)(l + 1) * p.n_tiles + tile) * A_BYTES;
+        bulk_s2g(dst, sA, A_BYTES);
+        bulk_commit();
+      }
+    }
+    if (!TRAIN) {
+      // a9 ray-chunk sum of M = mu0 (w_o . h_L + b_o) over the warp's 32 samples
+      float mu = p.mu0 * (mu_acc + sWo[H]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mu += __shfl_xor_sync(0xffffffffu, mu, o);
+      if (lane == 0 && valid) p.pchunk[g >> 5] = mu;
+    } else {
+      float us = u_row;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) us += __shfl_xor_sync(0xffffffffu, us, o);
+      bo_acc += us;
+      // ------------------------------------------------------------ a12 backward dX chain
+      for (int l = L - 1; l >= 1; --l) {
+        if (tid == 0) {
+          uint32_t wl = w_ready(l);
+          tc_fence_after();
+#pragma unroll 4
+          for (int kk = 0; kk < H / 16; ++kk) {
+            uint64_t ad = sdesc_sw128(a_base + (kk >> 2) * (128 * 128) + (kk & 3) * 32, 16, 1024);
+            uint64_t bd = sdesc_sw128(wl + kk * 2048, H * 128, 1024);  // MN-major W_l
+            umma_bf16(tmem, ad, bd, idesc_b, kk > 0 ? 1u : 0u);
+          }
+          umma_commit(mma_bar);
+        }
+        mbar_wait(mma_bar, mma_phase);
+        mma_phase ^= 1;
+        tc_fence_after();
+        if (tid == 0) {
+          if (!resident) {
+            int nxt = (l - 1 >= 1) ? l - 1 : 0;
+            bool has_next = (l - 1 >= 1) || more_tiles;
+            if (has_next && nxt != w_cur) w_issue(nxt);
+          }
+          bulk_wait_read_all();
+        }
+        __syncthreads();
+        const uint4 *zsrc = reinterpret_cast<const uint4 *>(p.zstash) + (((size_t)(l - 1) * p.n_tiles + tile) * (H / 8)) * 128 + row;
+#pragma unroll 1
+        for (int cb = 0; cb < H / 32; ++cb) {
+          uint32_t v[32];
+          tmem_ld32(tmem_row + cb * 32, v);
+          uint4 zq[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) zq[q] = zsrc[(size_t)(cb * 4 + q) * 128];
+          tmem_wait_ld();
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const uint32_t zz[4] = {zq[q].x, zq[q].y, zq[q].z, zq[q].w};
+            uint32_t w4[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              __half2 hh = *reinterpret_cast<const __half2 *>(&zz[e]);
+              float2 zf = __half22float2(hh);
+              int i0 = 8 * q + 2 * e;
+              w4[e] = pack_bf16x2(__uint_as_float(v[i0]) * dswish_f(zf.x), __uint_as_float(v[i0 + 1]) * dswish_f(zf.y));
+            }
+            st_shared_v4(a_base + sw128_offset(row, cb * 32 + 8 * q, 128), w4[0], w4[1], w4[2], w4[3]);
+          }
+        }
+        fence_proxy_async_smem();
+        tc_fence_before();
+        __syncthreads();
+        if (tid == 0) {
+          bulk_s2g(p.dstash + ((size_t)(l - 1) * p.n_tiles + tile) * A_BYTES, sA, A_BYTES);
+          bulk_commit();
+        }
+      }
+    }
+  }
+  if (TRAIN) {
+    // per-CTA head partials: [H] = dL/dw_o, [H] slot = dL/db_o; combine the 4 warps via smem
+    __syncthreads();
+    float *red = reinterpret_cast<float *>(sA);  // A tile is free now (all bulk reads waited below)
+    if (tid == 0) bulk_wait_read_all();
+    __syncthreads();
+#pragma unroll
+    for (int cb = 0; cb < H / 32; ++cb) red[warp * (H + 1) + cb * 32 + lane] = head_acc[cb];
+    if (lane == 0) red[warp * (H + 1) + H] = bo_acc;
+    __syncthreads();
+    for (int k = tid; k <= H; k += 128) {
+      float acc = 0.f;
+      for (int w = 0; w < 4; ++w) acc += red[w * (H + 1) + k];
+      p.head_part[(size_t)blockIdx.x * (H + 1) + k] = acc;
+    }
+    if (tid == 0) bulk_wait_all();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc(tmem, H);
+  }
+}
+
+}  // namespace dinr
