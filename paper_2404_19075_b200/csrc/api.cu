@@ -46,7 +46,7 @@ struct Launch {
   cudaStream_t st;
   cudaEvent_t a = nullptr, b = nullptr;
   Launch(dinr_ctx *c_, int cls_, cudaStream_t st_) : c(c_), cls(cls_), st(st_) {
-    c->launches++;
+    if (cls != T_AR) c->launches++;  // NCCL's kernel is not ours
     if (c->timing) {
       a = take();
       b = take();
