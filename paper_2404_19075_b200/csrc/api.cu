@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -19,6 +20,7 @@
 #include "k_small.cuh"
 #include "k_tc_dw.cuh"
 #include "k_tc_mlp.cuh"
+#include "k_fused.cuh"
 #include "nccl_dl.cuh"
 
 using namespace dinr;
@@ -94,6 +96,11 @@ struct Plan {
   int ksplit, nmb;
   int ksplit_simt;
   int nloss;
+  // fused training path (k_fused): nf top layers' dW in TMEM, nu = L - nf through K5
+  bool fused;
+  int nf, nu, grid_f, dw_layers;
+  uint8_t *ring;
+  float *dwf, *dbf;
   // carved pointers
   float4 *rec32;
   float *pchunk, *u, *fhat, *loss_part, *head_part, *dw_part, *db_part, *colsum;
@@ -102,6 +109,12 @@ struct Plan {
   int64_t *idx_dev;
   float *y_dev, *grad_dev;
 };
+
+bool use_fused(const dinr_ctx *c) {
+  static const bool off = std::getenv("DINR_NO_FUSED") != nullptr;
+  const int sn = c->S * c->geom.samples_per_ray;
+  return !off && c->field.precision == DINR_BF16 && c->H <= 128 && sn <= 256 && 256 % sn == 0;
+}
 
 int loss_blocks_for(int64_t n) { return (int)std::max<int64_t>(1, (n + kLossThreads - 1) / kLossThreads); }
 
@@ -140,7 +153,30 @@ size_t plan_layout(dinr_ctx *c, int64_t n, bool train, bool host_io, Plan &pl, v
     pl.dw_part = ar.take<float>((size_t)L * pl.nmb * ks * 128 * H);
     pl.db_part = ar.take<float>((size_t)L * pl.nmb * ks * 128);
   }
-  if (!simt && train) {
+  pl.fused = train && use_fused(c);
+  pl.nf = pl.nu = pl.grid_f = 0;
+  pl.dw_layers = L;
+  pl.ring = nullptr;
+  pl.dwf = pl.dbf = nullptr;
+  if (pl.fused) {
+    pl.nf = std::min(L, 512 / H - 1);
+    pl.nu = L - pl.nf;
+    pl.dw_layers = pl.nu;
+    const int64_t n_groups = (pl.nsamp + 255) / 256;
+    pl.grid_f = (int)std::max<int64_t>(1, std::min<int64_t>(n_groups, c->sm_count));
+    pl.ksplit = pl.nu > 0 ? (int)std::max<int64_t>(1, std::min<int64_t>(pl.n_tiles, (c->sm_count + pl.nu - 1) / pl.nu)) : 1;
+    pl.ring = ar.take<uint8_t>((size_t)pl.grid_f * 2 * (L + pl.nf) * H * 256);
+    pl.dwf = ar.take<float>((size_t)pl.nf * pl.grid_f * 128 * H);
+    pl.dbf = ar.take<float>((size_t)pl.nf * pl.grid_f * 128);
+    pl.head_part = ar.take<float>((size_t)pl.grid_f * (H + 1));
+    pl.loss_part = ar.take<float>((size_t)pl.grid_f + 1);
+    if (pl.nu > 0) {
+      pl.hstash = ar.take<uint8_t>((size_t)pl.nu * pl.n_tiles * H * 256);
+      pl.dstash = ar.take<uint8_t>((size_t)pl.nu * pl.n_tiles * H * 256);
+      pl.dw_part = ar.take<float>((size_t)pl.nu * pl.ksplit * 128 * H);
+      pl.db_part = ar.take<float>((size_t)pl.nu * pl.ksplit * 128);
+    }
+  } else if (!simt && train) {
     pl.hstash = ar.take<uint8_t>((size_t)L * pl.n_tiles * H * 256);
     pl.dstash = ar.take<uint8_t>((size_t)L * pl.n_tiles * H * 256);
     pl.zstash = ar.take<uint8_t>((size_t)std::max(1, L - 1) * pl.n_tiles * H * 256);
@@ -280,7 +316,42 @@ dinr_status launch_tc_dw(dinr_ctx *c, const Plan &pl, cudaStream_t st) {
   dinr_status s = set_smem(c, k_tc_dw<H>, smem);
   if (s) return s;
   Launch L_(c, T_DW, st);
-  k_tc_dw<H><<<dim3(pl.ksplit, pl.nmb, c->L), 128, smem, st>>>(p);
+  k_tc_dw<H><<<dim3(pl.ksplit, pl.nmb, pl.dw_layers), 128, smem, st>>>(p);
+  CUDA_TRY(c, cudaGetLastError());
+  return DINR_OK;
+}
+
+template <int H>
+dinr_status launch_fused(dinr_ctx *c, const Plan &pl, const float *y, cudaStream_t st) {
+  FusedParams p{};
+  p.rec32 = pl.rec32;
+  p.n_pix = pl.n;
+  p.nsamp = pl.nsamp;
+  p.n_s = c->geom.samples_per_ray;
+  p.S = c->S;
+  p.L = c->L;
+  p.nf = pl.nf;
+  p.combine = c->field.combine;
+  p.mu0 = (float)c->field.mu0;
+  p.inv_n = 1.f / (float)pl.n;
+  p.params = c->d_params;
+  p.B = c->d_B;
+  p.wpack_half = c->d_wpack_half;
+  p.y = y;
+  p.fhat = pl.fhat;
+  p.ring = pl.ring;
+  p.hstash = pl.hstash;
+  p.dstash = pl.dstash;
+  p.n_tiles = pl.n_tiles;
+  p.dw_part = pl.dwf;
+  p.db_part = pl.dbf;
+  p.head_part = pl.head_part;
+  p.loss_part = pl.loss_part;
+  size_t smem = FusedLayout<H>::smem_bytes(c->L);
+  dinr_status s = set_smem(c, k_fused<H>, smem);
+  if (s) return s;
+  Launch L_(c, T_BWD, st);
+  k_fused<H><<<pl.grid_f, FusedLayout<H>::NT, smem, st>>>(p);
   CUDA_TRY(c, cudaGetLastError());
   return DINR_OK;
 }
@@ -447,6 +518,20 @@ dinr_status step_grad(dinr_ctx *c, const int64_t *idx, int64_t n, const float *y
   }
   s = launch_rays(c, idx, n, nullptr, pl.rec32, st);
   if (s) return s;
+  if (pl.fused) {
+    s = c->H == 64 ? launch_fused<64>(c, pl, y, st) : launch_fused<128>(c, pl, y, st);
+    if (s) return s;
+    if (pl.nu > 0) {
+      s = tc_dw(c, pl, st);
+      if (s) return s;
+    }
+    Launch L_(c, T_ASM, st);
+    k_assemble2<<<(unsigned)((c->P + 1 + 255) / 256), 256, 0, st>>>(
+        c->H, c->L, c->P, pl.nu, pl.ksplit, pl.dw_part, pl.db_part, pl.grid_f, pl.dwf, pl.dbf, pl.head_part,
+        pl.grid_f, pl.loss_part, pl.grid_f, 1.f / (float)n, accumulate, grad);
+    CUDA_TRY(c, cudaGetLastError());
+    return DINR_OK;
+  }
   const bool simt = c->field.precision == DINR_FP32_VERIFY;
   if (simt) {
     s = simt_forward(c, pl, st);
@@ -538,6 +623,7 @@ dinr_status dinr_destroy(dinr_ctx *c) {
   cudaFree(c->d_B);
   cudaFree(c->d_params);
   cudaFree(c->d_wpack);
+  cudaFree(c->d_wpack_half);
   cudaFree(c->scratch);
   cudaFree(c->d_flags);
   delete c;
@@ -619,8 +705,11 @@ dinr_status dinr_set_field_weights(dinr_ctx *c, const dinr_field_desc *f, const 
   size_t wbytes = (size_t)L * H * H * 2;
   if (wbytes > c->wpack_cap) {
     cudaFree(c->d_wpack);
-    c->d_wpack = nullptr;
+    cudaFree(c->d_wpack_half);
+    c->d_wpack = c->d_wpack_half = nullptr;
+    c->wpack_cap = 0;
     CUDA_TRY(c, cudaMalloc(&c->d_wpack, wbytes));
+    CUDA_TRY(c, cudaMalloc(&c->d_wpack_half, wbytes));
     c->wpack_cap = wbytes;
   }
   if (!c->d_B || f->n_freq > c->C) {
@@ -638,7 +727,7 @@ dinr_status dinr_set_field_weights(dinr_ctx *c, const dinr_field_desc *f, const 
   if (f->precision == DINR_BF16) {
     Launch L_(c, T_PACK, st);
     int64_t tot = (int64_t)L * H * H;
-    k_pack_weights<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(c->d_params, H, L, c->d_wpack);
+    k_pack_weights<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(c->d_params, H, L, c->d_wpack, c->d_wpack_half);
   }
   CUDA_TRY(c, cudaGetLastError());
   c->have_field = true;

@@ -67,7 +67,8 @@ struct dinr_ctx {
   int64_t P = 0;
   float *d_B = nullptr;
   float *d_params = nullptr;
-  uint16_t *d_wpack = nullptr;
+  uint16_t *d_wpack = nullptr;       // bf16 SW128 images of W_l
+  uint16_t *d_wpack_half = nullptr;  // same, prescaled by 0.5 (fused kernel)
   size_t wpack_cap = 0, params_cap = 0;
 
   // scratch (grown on demand)

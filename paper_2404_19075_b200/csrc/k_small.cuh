@@ -13,7 +13,8 @@ namespace dinr {
 // The same image serves as the K-major B operand of the forward (N = out, K = in) and the
 // MN-major B operand of the backward dX GEMM (N = in, K = out).
 // ---------------------------------------------------------------------------------------
-__global__ void k_pack_weights(const float *__restrict__ params, int H, int L, uint16_t *__restrict__ wpack) {
+__global__ void k_pack_weights(const float *__restrict__ params, int H, int L, uint16_t *__restrict__ wpack,
+                               uint16_t *__restrict__ wpack_half) {
   int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int64_t per = (int64_t)H * H;
   if (q >= per * L) return;
@@ -22,8 +23,10 @@ __global__ void k_pack_weights(const float *__restrict__ params, int H, int L, u
   int o = e / H, i = e % H;
   float w = params[(int64_t)l * (per + H) + e];
   __nv_bfloat16 b = __float2bfloat16_rn(w);
+  __nv_bfloat16 bh = __float2bfloat16_rn(0.5f * w);  // exact: a power-of-two scale of a bf16 value
   uint32_t off = sw128_offset((uint32_t)o, (uint32_t)i, (uint32_t)H) >> 1;
   wpack[(int64_t)l * per + off] = *reinterpret_cast<uint16_t *>(&b);
+  wpack_half[(int64_t)l * per + off] = *reinterpret_cast<uint16_t *>(&bh);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -126,6 +129,43 @@ __global__ void k_assemble(int H, int L, int64_t P, int nmb, int ksplit, const f
     }
   } else {
     int k = (int)(q - (int64_t)L * per);  // 0..H-1 -> w_o, H -> b_o
+    for (int b = 0; b < nhead; ++b) v += head_part[(int64_t)b * (H + 1) + k];
+  }
+  grad[q] = accumulate ? grad[q] + v : v;
+}
+
+// Assembly for the fused path (H <= 128): layers [0, nu) from the dW GEMM partials
+// ([l][ks5][128][H]), layers [nu, L) from the fused kernel's per-CTA TMEM partials
+// ([l - nu][ksf][128][H]); fixed summation order -> deterministic.
+__global__ void k_assemble2(int H, int L, int64_t P, int nu, int ks5, const float *__restrict__ dw5,
+                            const float *__restrict__ db5, int ksf, const float *__restrict__ dwf,
+                            const float *__restrict__ dbf, const float *__restrict__ head_part, int nhead,
+                            const float *__restrict__ loss_part, int nloss, float inv_n, int accumulate,
+                            float *__restrict__ grad) {
+  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q > P) return;
+  float v = 0.f;
+  int64_t per = (int64_t)H * H + H;
+  if (q == P) {
+    for (int b = 0; b < nloss; ++b) v += loss_part[b];
+    v *= inv_n;
+  } else if (q < (int64_t)L * per) {
+    int l = (int)(q / per);
+    int64_t e = q - (int64_t)l * per;
+    const bool f = l >= nu;
+    const int ks = f ? ksf : ks5;
+    const int ll = f ? l - nu : l;
+    if (e < (int64_t)H * H) {
+      int o = (int)(e / H), i = (int)(e % H);
+      const float *src = (f ? dwf : dw5) + ((size_t)ll * ks * 128 + o) * H + i;
+      for (int s = 0; s < ks; ++s) v += src[(size_t)s * 128 * H];
+    } else {
+      int o = (int)(e - (int64_t)H * H);
+      const float *src = (f ? dbf : db5) + (size_t)ll * ks * 128 + o;
+      for (int s = 0; s < ks; ++s) v += src[(size_t)s * 128];
+    }
+  } else {
+    int k = (int)(q - (int64_t)L * per);
     for (int b = 0; b < nhead; ++b) v += head_part[(int64_t)b * (H + 1) + k];
   }
   grad[q] = accumulate ? grad[q] + v : v;
