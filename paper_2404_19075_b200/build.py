@@ -33,21 +33,27 @@ def needs_build() -> bool:
     return any(os.path.getmtime(s) > t for s in _sources())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, out: str = SO, defines=()) -> str:
+    if out == SO and not force and not needs_build():
         return SO
     cmd = [
         NVCC, "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
-        "-Xcompiler", "-fPIC,-O2", "-shared", "-o", SO + ".tmp", os.path.join(SRC_DIR, "api.cu"),
+        "-Xcompiler", "-fPIC,-O2", "-shared", "-o", out + ".tmp", os.path.join(SRC_DIR, "api.cu"),
         "-I", INC, "-ldl",
-    ]
+    ] + [f"-D{d}" for d in defines]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     subprocess.check_call(cmd)
-    os.replace(SO + ".tmp", SO)
-    return SO
+    os.replace(out + ".tmp", out)
+    return out
 
 
 if __name__ == "__main__":
-    build(force=True, verbose="--verbose" in sys.argv)
-    print(SO)
+    if "--phases" in sys.argv:  # debug variant with per-phase cycle counters in k_fused
+        extra = [a[2:] for a in sys.argv if a.startswith("-D")]
+        tag = "_".join(e.lower().replace("dinr_exp_", "") for e in extra)
+        print(build(force=True, out=os.path.join(HERE, f"libdinr_phases{('_' + tag) if tag else ''}.so"),
+                    defines=["DINR_PHASES"] + extra))
+    else:
+        build(force=True, verbose="--verbose" in sys.argv)
+        print(SO)

@@ -350,9 +350,32 @@ dinr_status launch_fused(dinr_ctx *c, const Plan &pl, const float *y, cudaStream
   size_t smem = FusedLayout<H>::smem_bytes(c->L);
   dinr_status s = set_smem(c, k_fused<H>, smem);
   if (s) return s;
-  Launch L_(c, T_BWD, st);
-  k_fused<H><<<pl.grid_f, FusedLayout<H>::NT, smem, st>>>(p);
+#ifdef DINR_PHASES
+  static unsigned long long *dbg = nullptr;
+  if (!dbg) cudaMalloc(&dbg, sizeof(unsigned long long) * 8 * 1024);
+  cudaMemsetAsync(dbg, 0, sizeof(unsigned long long) * 8 * 1024, st);
+  p.dbg = dbg;
+#endif
+  {
+    Launch L_(c, T_BWD, st);
+    k_fused<H><<<pl.grid_f, FusedLayout<H>::NT, smem, st>>>(p);
+  }
   CUDA_TRY(c, cudaGetLastError());
+#ifdef DINR_PHASES
+  {
+    std::vector<unsigned long long> h((size_t)pl.grid_f * 8);
+    cudaStreamSynchronize(st);
+    cudaMemcpy(h.data(), dbg, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost);
+    double tot[8] = {0};
+    for (int b = 0; b < pl.grid_f; ++b)
+      for (int k = 0; k < 8; ++k) tot[k] += (double)h[(size_t)b * 8 + k];
+    const double tiles = (double)pl.n_tiles;
+    std::fprintf(stderr, "[dinr phases] cycles per tile (CTA-avg): feat %.0f fwd_epi %.0f fwd_wait %.0f last+loss %.0f "
+                         "bwd_epi %.0f bwd_wait %.0f bwd_pre %.0f\n",
+                 tot[0] / tiles, tot[2] / tiles, tot[1] / tiles, tot[3] / tiles, tot[4] / tiles, tot[5] / tiles,
+                 tot[6] / tiles);
+  }
+#endif
   return DINR_OK;
 }
 

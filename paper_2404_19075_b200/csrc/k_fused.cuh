@@ -37,6 +37,7 @@ struct FusedParams {
   float *db_part;         // [nf][grid][128]
   float *head_part;       // [grid][H+1]
   float *loss_part;       // [grid]
+  unsigned long long *dbg;  // DINR_PHASES builds: [grid][8] cycle counters
 };
 
 template <int H>
@@ -53,6 +54,21 @@ struct FusedLayout {
   }
 };
 
+#ifdef DINR_PHASES
+#define PH_MARK(k)                        \
+  do {                                    \
+    if (tid == 0) {                       \
+      unsigned long long _t = clock64();  \
+      ph[k] += _t - ph_last;              \
+      ph_last = _t;                       \
+    }                                     \
+  } while (0)
+#else
+#define PH_MARK(k) \
+  do {             \
+  } while (0)
+#endif
+
 __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
 template <int H>
@@ -63,7 +79,7 @@ __global__ void __launch_bounds__(FusedLayout<H>::NT, 1) k_fused(FusedParams p) 
   constexpr int EPI = LY::EPI;
   constexpr uint32_t TILE = LY::TILE;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // keeps the shared address space
   const int L = p.L, nf = p.nf, nu = L - nf;  // unfused layers: 0..nu-1
   uint8_t *sA = smem;
   uint8_t *sHB = sA + LY::A_BYTES;
@@ -77,8 +93,8 @@ __global__ void __launch_bounds__(FusedLayout<H>::NT, 1) k_fused(FusedParams p) 
   float *sP = sU + 64;                   // [8] chunk sums of M
   float *sMisc = sP + 64;                // [warps] loss partials
   uint64_t *bars = reinterpret_cast<uint64_t *>(sMisc + 64);
-  uint64_t *a_full = bars, *acc_full = bars + 1, *w_bar = bars + 2, *hb_bar = bars + 3;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 4);
+  uint64_t *a_full = bars, *acc_full = bars + 1, *w_bar = bars + 2, *hb_bar = bars + 3, *sa_free = bars + 4;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 5);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const bool ctrl = (tid >= EPI);
@@ -91,6 +107,7 @@ __global__ void __launch_bounds__(FusedLayout<H>::NT, 1) k_fused(FusedParams p) 
     mbar_init(acc_full, 1);
     mbar_init(w_bar, 1);
     mbar_init(hb_bar, 1);
+    mbar_init(sa_free, 1);
     fence_mbar_init();
   }
   const int64_t per = (int64_t)H * H + H;
@@ -123,10 +140,17 @@ __global__ void __launch_bounds__(FusedLayout<H>::NT, 1) k_fused(FusedParams p) 
       uint32_t aph = 0, hph = 0, ncommit = 0, dw_init = 0;
       for (int64_t gi = blockIdx.x; gi < n_groups; gi += gridDim.x) {
         for (int s = 0; s < 2; ++s) {
+          const int64_t tile = 2 * gi + s;
           for (int l = 0; l < L; ++l) {
             mbar_wait(a_full, aph);
             aph ^= 1;
             tc_fence_after();
+            // h_l (the A tile) is an operand of dW_l: fused -> L2 ring, unfused -> dW GEMM stash
+            if (l >= nu)
+              bulk_s2g_hint(ring_h(s, l - nu), sA, TILE, pol_keep);
+            else
+              bulk_s2g_hint(p.hstash + ((size_t)l * p.n_tiles + tile) * TILE, sA, TILE, pol_stream);
+            bulk_commit();
             const uint32_t wl = w_base + (uint32_t)l * LY::W_LAYER;
 #pragma unroll
             for (int kk = 0; kk < H / 16; ++kk)
@@ -134,10 +158,13 @@ __global__ void __launch_bounds__(FusedLayout<H>::NT, 1) k_fused(FusedParams p) 
                         sdesc_sw128(wl + (kk >> 2) * (H * 128) + (kk & 3) * 32, 16, 1024), idf, kk > 0);
             umma_commit(acc_full);
             ++ncommit;
+            bulk_wait_read_all();  // the copy engine is done with sA
+            mbar_arrive(sa_free);
           }
         }
         // backward (the loss runs on the epilogue warps in between)
         for (int s = 0; s < 2; ++s) {
+          const int64_t tile = 2 * gi + s;
           for (int l = L - 1; l >= 0; --l) {
             const bool fused = l >= nu;
             if (fused) {  // prefetch h_l into HB (HB is free: the previous dW MMA retired)
@@ -147,6 +174,10 @@ __global__ void __launch_bounds__(FusedLayout<H>::NT, 1) k_fused(FusedParams p) 
             mbar_wait(a_full, aph);
             aph ^= 1;
             tc_fence_after();
+            if (!fused) {  // delta_l image for the dW GEMM
+              bulk_s2g_hint(p.dstash + ((size_t)l * p.n_tiles + tile) * TILE, sA, TILE, pol_stream);
+              bulk_commit();
+            }
             if (fused) {
               mbar_wait(hb_bar, hph);
               hph ^= 1;
@@ -168,6 +199,8 @@ __global__ void __launch_bounds__(FusedLayout<H>::NT, 1) k_fused(FusedParams p) 
             }
             umma_commit(acc_full);
             ++ncommit;
+            bulk_wait_read_all();
+            mbar_arrive(sa_free);
             // HB is reused by the next fused layer: wait until this dW MMA has retired
             if (fused) mbar_wait(acc_full, (ncommit - 1) & 1);
           }
@@ -182,6 +215,18 @@ __global__ void __launch_bounds__(FusedLayout<H>::NT, 1) k_fused(FusedParams p) 
     const int col0 = cg * 32;
     const uint32_t trow = tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)col0;
     uint32_t accph = 0;
+    uint32_t sfph = 0;
+    bool sf_first = true;
+    auto wait_sa = [&]() {  // the copy engine has finished reading sA for the previous step
+      if (!sf_first) {
+        mbar_wait(sa_free, sfph);
+        sfph ^= 1;
+      }
+      sf_first = false;
+    };
+#ifdef DINR_PHASES
+    unsigned long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0}, ph_last = clock64();
+#endif
     float dbacc[4] = {0.f, 0.f, 0.f, 0.f};  // fused-layer bias gradients (lane = column)
     float wo_acc = 0.f;                      // dL/dw_o partial (warps with warp % 4 == 0)
     float bo_acc = 0.f, loss_acc = 0.f;
@@ -206,9 +251,11 @@ __global__ void __launch_bounds__(FusedLayout<H>::NT, 1) k_fused(FusedParams p) 
             rb2 = ra.y + jj * rv.y;
             rb3 = ra.x + jj * rv.x;
           }
+          constexpr int NCH = (C / CG) / 8;  // 8-frequency chunks per thread
+          uint32_t pc[NCH][4], ps[NCH][4];
 #pragma unroll
-          for (int c0 = cg * (C / CG); c0 < (cg + 1) * (C / CG); c0 += 8) {
-            uint32_t pc[4], ps[4];
+          for (int ch = 0; ch < NCH; ++ch) {
+            const int c0 = cg * (C / CG) + 8 * ch;
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
               float cs[2], sn[2];
@@ -219,31 +266,27 @@ __global__ void __launch_bounds__(FusedLayout<H>::NT, 1) k_fused(FusedParams p) 
                 float fr = phi - rintf(phi);
                 __sincosf(6.283185307179586f * fr, &sn[e], &cs[e]);
               }
-              pc[q] = pack_bf16x2(cs[0], cs[1]);
-              ps[q] = pack_bf16x2(sn[0], sn[1]);
+              pc[ch][q] = pack_bf16x2(cs[0], cs[1]);
+              ps[ch][q] = pack_bf16x2(sn[0], sn[1]);
             }
-            st_shared_v4(a_base + sw128_offset(row, c0, 128), pc[0], pc[1], pc[2], pc[3]);
-            st_shared_v4(a_base + sw128_offset(row, C + c0, 128), ps[0], ps[1], ps[2], ps[3]);
+          }
+          wait_sa();
+#pragma unroll
+          for (int ch = 0; ch < NCH; ++ch) {
+            const int c0 = cg * (C / CG) + 8 * ch;
+            st_shared_v4(a_base + sw128_offset(row, c0, 128), pc[ch][0], pc[ch][1], pc[ch][2], pc[ch][3]);
+            st_shared_v4(a_base + sw128_offset(row, C + c0, 128), ps[ch][0], ps[ch][1], ps[ch][2], ps[ch][3]);
           }
         }
         fence_proxy_async_smem();
         mbar_arrive(a_full);
-        {  // h_0 image for the dW GEMM / ring (copied out of sA after the arrive; sA is read-only now)
-          uint8_t *img = nu > 0 ? p.hstash + ((size_t)0 * p.n_tiles + tile) * TILE : ring_h(s, 0);
-          const uint64_t pol = nu > 0 ? pol_stream : pol_keep;
-#pragma unroll
-          for (int c0 = cg * (C / CG); c0 < (cg + 1) * (C / CG); c0 += 8) {
-            uint4 a, b;
-            asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w) : "r"(a_base + sw128_offset(row, c0, 128)));
-            asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w) : "r"(a_base + sw128_offset(row, C + c0, 128)));
-            st_global_v4_hint(img + sw128_offset(row, c0, 128), a, pol);
-            st_global_v4_hint(img + sw128_offset(row, C + c0, 128), b, pol);
-          }
-        }
+        PH_MARK(0);
         float mu_part = 0.f;
         for (int l = 0; l < L; ++l) {
           const bool last = (l == L - 1);
+          PH_MARK(2);
           mbar_wait(acc_full, accph);
+          PH_MARK(1);
           accph ^= 1;
           tc_fence_after();
           uint32_t hpk[16], s2k[16];  // packed bf16x2 results for this thread's 32 columns
@@ -269,24 +312,22 @@ __global__ void __launch_bounds__(FusedLayout<H>::NT, 1) k_fused(FusedParams p) 
           }
           tc_fence_before();
           if (!last) {
+            wait_sa();
 #pragma unroll
             for (int q = 0; q < 4; ++q)
               st_shared_v4(a_base + sw128_offset(row, col0 + 8 * q, 128), hpk[4 * q], hpk[4 * q + 1], hpk[4 * q + 2], hpk[4 * q + 3]);
+#ifndef DINR_EXP_NO_FENCE
             fence_proxy_async_smem();
+#endif
             mbar_arrive(a_full);
-            // global copies after the arrive, so the next MMA is not held up by them
-            uint8_t *img = (l + 1 < nu) ? p.hstash + ((size_t)(l + 1) * p.n_tiles + tile) * TILE : ring_h(s, l + 1 - nu);
-            const uint64_t pol = (l + 1 < nu) ? pol_stream : pol_keep;
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-              st_global_v4_hint(img + sw128_offset(row, col0 + 8 * q, 128),
-                                make_uint4(hpk[4 * q], hpk[4 * q + 1], hpk[4 * q + 2], hpk[4 * q + 3]), pol);
           }
+#ifndef DINR_EXP_NO_S2_STORE
           uint4 *s2dst = reinterpret_cast<uint4 *>(ring_s2(s, l));
 #pragma unroll
           for (int q = 0; q < 4; ++q)
             st_global_v4_hint(s2dst + (size_t)((col0 >> 3) + q) * 128 + row,
                               make_uint4(s2k[4 * q], s2k[4 * q + 1], s2k[4 * q + 2], s2k[4 * q + 3]), pol_keep);
+#endif
           if (last) {
             float hv[32];
 #pragma unroll
@@ -370,6 +411,7 @@ __global__ void __launch_bounds__(FusedLayout<H>::NT, 1) k_fused(FusedParams p) 
         }
       }
       named_sync(1, EPI);
+      PH_MARK(3);
       // head gradients: dL/dw_o += sum_chunks u_chunk hsum_chunk, dL/db_o += sum u over samples
       if ((warp & 3) == 0) {
         float a = 0.f;
@@ -393,7 +435,9 @@ __global__ void __launch_bounds__(FusedLayout<H>::NT, 1) k_fused(FusedParams p) 
 #pragma unroll
           for (int q = 0; q < 4; ++q) sq[q] = ld_global_v4_hint(s2src + (size_t)((col0 >> 3) + q) * 128 + row, pol_stream);
           if (!top) {
+            PH_MARK(6);
             mbar_wait(acc_full, accph);
+            PH_MARK(5);
             accph ^= 1;
             tc_fence_after();
           }
@@ -420,18 +464,14 @@ __global__ void __launch_bounds__(FusedLayout<H>::NT, 1) k_fused(FusedParams p) 
             }
           }
           tc_fence_before();
+          wait_sa();
 #pragma unroll
           for (int q = 0; q < 4; ++q)
             st_shared_v4(a_base + sw128_offset(row, col0 + 8 * q, 128), dp[4 * q], dp[4 * q + 1], dp[4 * q + 2], dp[4 * q + 3]);
           fence_proxy_async_smem();
           mbar_arrive(a_full);
-          if (l < nu) {  // unfused: delta image for the dW GEMM, streamed out
-            uint8_t *dimg = p.dstash + ((size_t)l * p.n_tiles + (2 * gi + s)) * TILE;
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-              st_global_v4_hint(dimg + sw128_offset(row, col0 + 8 * q, 128),
-                                make_uint4(dp[4 * q], dp[4 * q + 1], dp[4 * q + 2], dp[4 * q + 3]), pol_stream);
-          } else {  // db of a fused layer: column sums of delta over the warp's 32 rows
+          PH_MARK(4);
+          if (l >= nu) {  // db of a fused layer: column sums of delta over the warp's 32 rows
             float d[32];
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
@@ -455,11 +495,16 @@ __global__ void __launch_bounds__(FusedLayout<H>::NT, 1) k_fused(FusedParams p) 
         }
         // the l = 0 step (dW MMA or delta_0 store) must retire before sA is rewritten
         mbar_wait(acc_full, accph);
+        PH_MARK(5);
         accph ^= 1;
         tc_fence_after();
       }
     }
     // ------------------------------------------------------------ flush per-CTA partials
+#ifdef DINR_PHASES
+    if (tid == 0 && p.dbg)
+      for (int k = 0; k < 8; ++k) p.dbg[(size_t)blockIdx.x * 8 + k] = ph[k];
+#endif
     named_sync(1, EPI);
     for (int j = 0; j < nf; ++j) {
       uint32_t v[32];

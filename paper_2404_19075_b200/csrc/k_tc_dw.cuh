@@ -37,7 +37,7 @@ __global__ void __launch_bounds__(128, 1) k_tc_dw(DwParams p) {
   using LY = DwLayout<H>;
   constexpr int NST = LY::NST;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // keeps the shared address space
   uint8_t *ones = smem + NST * LY::STAGE;
   uint64_t *full = reinterpret_cast<uint64_t *>(ones + 2048);
   uint64_t *empty = full + NST;

@@ -63,7 +63,7 @@ __global__ void __launch_bounds__(128, 1) k_tc_mlp(TcParams p) {
   constexpr uint32_t A_BYTES = TcLayout<H>::A_BYTES;
   constexpr uint32_t W_LAYER = TcLayout<H>::W_LAYER;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // keeps the shared address space
   const int L = p.L;
   const bool resident = p.resident != 0;
   uint8_t *sA = smem;
