@@ -6,8 +6,9 @@
 One step = the whole north_star hot path over one per-GPU batch of B_px pixels (BASELINE
 workload, synthetic seeded inputs resident in HBM): ray setup (K1), fused forward MLP
 projection (K2), combine + loss (K4), fused recomputed forward + backward dX chain (K3), dW
-GEMM (K5), gradient assembly, NCCL all-reduce of the gradient (ncclAvg), and the bf16 weight
-re-pack of set_field_weights.  Multi-GPU: launched by torchrun, one rank per GPU, views
+GEMM (K5), gradient assembly, NCCL all-reduce of the gradient (ncclAvg), and the Adam update
+fused with the re-pack of the bf16 weight images (NEXT row N1).  For pixel groups that fit two
+128-sample tiles (fan512, parallel64) the forward, loss and backward run as one fused kernel.  Multi-GPU: launched by torchrun, one rank per GPU, views
 sharded round-robin (weak scaling: B_px fixed per GPU).
 
 Timing: L2 is flushed (256 MiB write) before every step outside the timed intervals; each
@@ -243,10 +244,17 @@ def main():
     grad = torch.zeros(P + 1, device=dev)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
 
+    adam_m = torch.zeros(P, device=dev)
+    adam_v = torch.zeros(P, device=dev)
+    adam_t = [0]
+
     def step(q):
+        # one training step: local loss + gradient, gradient average across the
+        # ranks, then Adam (lr 1e-3) fused with the re-pack of the bf16 weight images
         D.project_and_grad(ctx, idx_pool[q % pool], y_pool[q % pool], grad, stream=stream)
         D.allreduce_grads(ctx, grad, stream=stream)
-        D.set_field_weights(ctx, f, B, params, stream=stream)
+        adam_t[0] += 1
+        D.adam_step(ctx, params, grad, adam_m, adam_v, lr=1e-3, step=adam_t[0], stream=stream)
 
     clk = ClockSampler(local)
     time.sleep(0.5)
@@ -323,10 +331,12 @@ def main():
         fps = flops_per_sample(L, H)
         # per-kernel algorithmic work per launch
         nsamp = n * S * ns
+        fused = ktimes["forward"][1] == 0  # k_fused: forward + loss + dX + top-nf dW in one kernel
+        nf = min(L, 512 // H - 1) if fused else 0
         alg = {
             "forward": ("tensor", 2.0 * L * H * H * nsamp),
-            "backward": ("tensor", 2.0 * (L - 1) * H * H * nsamp),
-            "dw": ("tensor", 2.0 * L * H * H * nsamp),
+            "backward": ("tensor", 2.0 * ((L + (L - 1) + nf) if fused else (L - 1)) * H * H * nsamp),
+            "dw": ("tensor", 2.0 * (L - nf) * H * H * nsamp),
             "rays": ("hbm", n * (8 + S * 32.0)),
             "loss": ("hbm", n * (4 + 4 + S * (32 + 4.0 * (ns // 32)) + S * 4)),
         }

@@ -150,6 +150,17 @@ dinr_status dinr_project_and_grad_host(dinr_ctx *ctx, const int64_t *idx_host, i
                                        const float *y_host, float *grad_host, int allreduce,
                                        void *stream);
 
+/* Optimizer step (NEXT row N1; "We use the Adam optimizer"):
+ * one fused kernel updates params_dev in place with Adam (bias-corrected, step >= 1),
+ *   m <- b1 m + (1-b1) g, v <- b2 v + (1-b2) g^2, p <- p - lr mhat/(sqrt(vhat)+eps),
+ * and re-packs the context's bf16 tensor-core weight images from the new values (so it
+ * replaces dinr_set_field_weights after the first call).  params_dev, m_dev, v_dev: P fp32
+ * each (D5 layout, caller-owned); grad_dev: at least P fp32 (slot P, the loss, is ignored).
+ * Requires dinr_set_field_weights first (DINR_ESTATE); count must equal P (DINR_EINVAL). */
+dinr_status dinr_adam_step(dinr_ctx *ctx, float *params_dev, const float *grad_dev, float *m_dev, float *v_dev,
+                           int64_t count, double lr, double beta1, double beta2, double eps, int64_t step,
+                           void *stream);
+
 /* fp64 ray records of kernel K1 (geometry / ray setup) for n pixels: rec_dev[n*S*9] =
  * {o.x,o.y,o.z, d.x,d.y,d.z, delta_min, delta_max, chord} per sub-ray, where o is the
  * rotated source, d = rotated detector point - o, [delta_min, delta_max] the FOV bounds

@@ -595,3 +595,14 @@ int or_project_exact(const or_geom *g, const double *theta, const double *t, int
   }
   return err ? -1 : 0;
 }
+
+void or_adam_step(double *param, const double *grad, double *m, double *v, int64_t n, double lr, double b1,
+                  double b2, double eps, int64_t step) {
+  double c1 = 1.0 - pow(b1, (double)step), c2 = 1.0 - pow(b2, (double)step);
+  for (int64_t q = 0; q < n; ++q) {
+    m[q] = b1 * m[q] + (1.0 - b1) * grad[q];
+    v[q] = b2 * v[q] + (1.0 - b2) * grad[q] * grad[q];
+    double mh = m[q] / c1, vh = v[q] / c2;
+    param[q] -= lr * mh / (sqrt(vh) + eps);
+  }
+}

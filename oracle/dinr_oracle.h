@@ -113,6 +113,12 @@ int or_project_exact(const or_geom *g, const double *theta, const double *t, int
                      int32_t combine, const or_prim *prims, int32_t n_prims,
                      const int64_t *idx, int64_t n, double *fhat, double *p_sub);
 
+/* Adam ("We use the Adam optimizer"; constants and bias correction as SPEC S:377-383):
+ * m <- b1 m + (1-b1) g; v <- b2 v + (1-b2) g^2; param -= lr * mhat / (sqrt(vhat) + eps),
+ * mhat = m / (1 - b1^step), vhat = v / (1 - b2^step), step >= 1 (in place, n values). */
+void or_adam_step(double *param, const double *grad, double *m, double *v, int64_t n, double lr, double b1,
+                  double b2, double eps, int64_t step);
+
 #ifdef __cplusplus
 }
 #endif

@@ -76,6 +76,7 @@ def lib():
         _lib.or_project_and_grad.argtypes = [C.POINTER(OrGeom), d, d, i64, C.POINTER(OrField), d, d, pi64, i64, d, d]
         _lib.or_project_analytic.argtypes = [C.POINTER(OrGeom), d, d, i64, i32, C.POINTER(OrPrim), i32, pi64, i64, d, d]
         _lib.or_project_exact.argtypes = [C.POINTER(OrGeom), d, d, i64, i32, C.POINTER(OrPrim), i32, pi64, i64, d, d]
+        _lib.or_adam_step.argtypes = [d, d, d, d, i64, C.c_double, C.c_double, C.c_double, C.c_double, i64]
         _lib.or_line_integral_exact.restype = C.c_double
         _lib.or_line_integral_exact.argtypes = [C.POINTER(OrPrim), i32, d, d, C.c_double, C.c_double, C.c_double]
     return _lib
@@ -226,3 +227,11 @@ def allreduce_mean(grads):
     for g_ in grads:
         acc = acc + np.asarray(g_, dtype=np.float64)
     return acc / len(grads)
+
+
+def adam_step(param, grad, m, v, lr, b1=0.9, b2=0.999, eps=1e-8, step=1):
+    """In place on float64 copies; returns (param, m, v)."""
+    pr, mm, vv = _f64(param).copy(), _f64(m).copy(), _f64(v).copy()
+    gg = _f64(grad)
+    lib().or_adam_step(_dp(pr), _dp(gg), _dp(mm), _dp(vv), len(pr), lr, b1, b2, eps, step)
+    return pr, mm, vv

@@ -28,7 +28,7 @@ EXPORTS = [
     "dinr_set_geometry", "dinr_set_field_weights", "dinr_project", "dinr_project_and_grad",
     "dinr_project_and_grad_host", "dinr_ray_records", "dinr_nccl_unique_id", "dinr_comm_init",
     "dinr_allreduce_grads", "dinr_get_device_status", "dinr_set_timing", "dinr_read_timing",
-    "dinr_launch_count",
+    "dinr_launch_count", "dinr_adam_step",
 ]
 
 
@@ -96,6 +96,7 @@ def load(path: str = SO_PATH):
         "dinr_set_timing": (st, [vp, C.c_int]),
         "dinr_read_timing": (st, [vp, C.c_int, d, C.POINTER(C.c_int64), C.c_int]),
         "dinr_launch_count": (i64, [vp]),
+        "dinr_adam_step": (st, [vp, vp, vp, vp, vp, i64, C.c_double, C.c_double, C.c_double, C.c_double, i64, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -178,6 +179,12 @@ def project_and_grad_host(ctx, idx_host, y_host, grad_host, allreduce: bool = Fa
     n = idx_host.numel() if hasattr(idx_host, "numel") else len(idx_host)
     _check(ctx, load().dinr_project_and_grad_host(ctx, hp(idx_host), n, hp(y_host), hp(grad_host), int(allreduce),
                                                   _stream(stream)))
+
+
+def adam_step(ctx, params, grad, m, v, lr, step, beta1=0.9, beta2=0.999, eps=1e-8, stream=None):
+    """N1: fused Adam update of params (in place) + re-pack of the bf16 weight images."""
+    _check(ctx, load().dinr_adam_step(ctx, _ptr(params), _ptr(grad), _ptr(m), _ptr(v), params.numel(), lr, beta1,
+                                      beta2, eps, step, _stream(stream, params)))
 
 
 def ray_records(ctx, idx, rec, stream=None):

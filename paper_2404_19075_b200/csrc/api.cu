@@ -112,8 +112,8 @@ struct Plan {
 
 bool use_fused(const dinr_ctx *c) {
   static const bool off = std::getenv("DINR_NO_FUSED") != nullptr;
-  const int sn = c->S * c->geom.samples_per_ray;
-  return !off && c->field.precision == DINR_BF16 && c->H <= 128 && sn <= 256 && 256 % sn == 0;
+  const int ns = c->geom.samples_per_ray, sn = c->S * ns;
+  return !off && c->field.precision == DINR_BF16 && c->H <= 128 && sn <= 256 && 256 % sn == 0 && (ns & (ns - 1)) == 0;
 }
 
 int loss_blocks_for(int64_t n) { return (int)std::max<int64_t>(1, (n + kLossThreads - 1) / kLossThreads); }
@@ -328,6 +328,8 @@ dinr_status launch_fused(dinr_ctx *c, const Plan &pl, const float *y, cudaStream
   p.n_pix = pl.n;
   p.nsamp = pl.nsamp;
   p.n_s = c->geom.samples_per_ray;
+  p.lg_ns = 0;
+  while ((1 << p.lg_ns) < p.n_s) ++p.lg_ns;
   p.S = c->S;
   p.L = c->L;
   p.nf = pl.nf;
@@ -754,6 +756,24 @@ dinr_status dinr_set_field_weights(dinr_ctx *c, const dinr_field_desc *f, const 
   }
   CUDA_TRY(c, cudaGetLastError());
   c->have_field = true;
+  return DINR_OK;
+}
+
+dinr_status dinr_adam_step(dinr_ctx *c, float *params, const float *grad, float *m, float *v, int64_t count,
+                           double lr, double b1, double b2, double eps, int64_t step, void *stream) {
+  if (!c) return DINR_EINVAL;
+  if (!c->have_field) return fail(c, DINR_ESTATE, "dinr_set_field_weights must be called first");
+  if (!params || !grad || !m || !v || count != c->P || step < 1 || !(lr >= 0) || !(b1 >= 0 && b1 < 1) ||
+      !(b2 >= 0 && b2 < 1) || !(eps > 0))
+    return fail(c, DINR_EINVAL, "bad Adam arguments (count must equal P, step >= 1, 0 <= beta < 1, eps > 0)");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const float c1 = (float)(1.0 - std::pow(b1, (double)step)), c2 = (float)(1.0 - std::pow(b2, (double)step));
+  Launch L_(c, T_PACK, st);
+  k_adam_pack<<<(unsigned)((c->P + 255) / 256), 256, 0, st>>>(params, grad, m, v, c->P, c->H, c->L, (float)lr,
+                                                              (float)b1, (float)b2, (float)eps, c1, c2, c->d_params,
+                                                              c->d_wpack, c->d_wpack_half);
+  CUDA_TRY(c, cudaGetLastError());
   return DINR_OK;
 }
 

@@ -22,7 +22,7 @@ namespace dinr {
 struct FusedParams {
   const float4 *rec32;
   int64_t n_pix, nsamp;
-  int n_s, S, L, nf;      // nf = number of top layers whose dW is fused in TMEM
+  int n_s, lg_ns, S, L, nf;  // nf = number of top layers whose dW is fused in TMEM
   int combine;
   float mu0, inv_n;
   const float *params;    // fp32 D5
@@ -213,13 +213,16 @@ __global__ void __launch_bounds__(FusedLayout<H>::NT, 1) k_fused(FusedParams p) 
     // ===================================================== epilogue warps
     const int row = tid & 127, cg = tid >> 7;
     const int col0 = cg * 32;
+    uint32_t aoff[4];  // SW128 byte offsets of this thread's four 16-B chunks in a tile image
+#pragma unroll
+    for (int q = 0; q < 4; ++q) aoff[q] = sw128_offset(row, col0 + 8 * q, 128);
     const uint32_t trow = tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)col0;
     uint32_t accph = 0;
     uint32_t sfph = 0;
     bool sf_first = true;
     auto wait_sa = [&]() {  // the copy engine has finished reading sA for the previous step
       if (!sf_first) {
-        mbar_wait(sa_free, sfph);
+        mbar_wait_sleep(sa_free, sfph);
         sfph ^= 1;
       }
       sf_first = false;
@@ -243,8 +246,8 @@ __global__ void __launch_bounds__(FusedLayout<H>::NT, 1) k_fused(FusedParams p) 
         {  // a5/a6: sample point, normalization and GRFF features of this thread's 16 frequencies
           float rb0 = 0.f, rb1 = 0.f, rb2 = 0.f, rb3 = 0.f;
           if (valid) {
-            int64_t ray = g / p.n_s;
-            float jj = (float)(g - ray * p.n_s) + 0.5f;
+            const int64_t ray = g >> p.lg_ns;  // N_s is a power of two on this path
+            float jj = (float)(g & (p.n_s - 1)) + 0.5f;
             float4 ra = p.rec32[2 * ray], rv = p.rec32[2 * ray + 1];
             rb0 = ra.w;
             rb1 = ra.z + jj * rv.z;
@@ -285,7 +288,7 @@ __global__ void __launch_bounds__(FusedLayout<H>::NT, 1) k_fused(FusedParams p) 
         for (int l = 0; l < L; ++l) {
           const bool last = (l == L - 1);
           PH_MARK(2);
-          mbar_wait(acc_full, accph);
+          mbar_wait_sleep(acc_full, accph);
           PH_MARK(1);
           accph ^= 1;
           tc_fence_after();
@@ -315,7 +318,7 @@ __global__ void __launch_bounds__(FusedLayout<H>::NT, 1) k_fused(FusedParams p) 
             wait_sa();
 #pragma unroll
             for (int q = 0; q < 4; ++q)
-              st_shared_v4(a_base + sw128_offset(row, col0 + 8 * q, 128), hpk[4 * q], hpk[4 * q + 1], hpk[4 * q + 2], hpk[4 * q + 3]);
+              st_shared_v4(a_base + aoff[q], hpk[4 * q], hpk[4 * q + 1], hpk[4 * q + 2], hpk[4 * q + 3]);
 #ifndef DINR_EXP_NO_FENCE
             fence_proxy_async_smem();
 #endif
@@ -356,19 +359,15 @@ __global__ void __launch_bounds__(FusedLayout<H>::NT, 1) k_fused(FusedParams p) 
       // ------------------------------------------------------------ a9-a11: combine + loss
       fence_proxy_async_global();  // ring h images (generic stores) are read back by TMA below
       named_sync(1, EPI);
-      if (tid < 8) {  // chunk sums of M = mu0 (w_o . h_L + b_o) over 32 samples
-        const int ss = tid >> 2, w4 = tid & 3;
-        float a = 0.f;
-        for (int r = 0; r < 32; ++r) {
-          const int rr = w4 * 32 + r;
-          if ((2 * gi + ss) * 128 + rr < p.nsamp) {
-            float m = sWo[H];
+      if (warp < 8) {  // a9: chunk sums of M = mu0 (w_o . h_L + b_o), warp q <-> 32-sample chunk q
+        const int ss = warp >> 2, rr = (warp & 3) * 32 + lane;
+        float m = sWo[H];
 #pragma unroll
-            for (int c = 0; c < CG; ++c) m += sMu[(ss * 128 + rr) * CG + c];
-            a += p.mu0 * m;
-          }
-        }
-        sP[tid] = a;
+        for (int c = 0; c < CG; ++c) m += sMu[(ss * 128 + rr) * CG + c];
+        float a = ((2 * gi + ss) * 128 + rr < p.nsamp) ? p.mu0 * m : 0.f;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+        if (lane == 0) sP[warp] = a;
       }
       named_sync(1, EPI);
       if (tid < pix_per_group) {
@@ -426,17 +425,18 @@ __global__ void __launch_bounds__(FusedLayout<H>::NT, 1) k_fused(FusedParams p) 
         bo_acc += a;
       }
       // ------------------------------------------------------------ a12: backward, two tiles
+      uint4 sq[4];  // s2 of the current backward step, prefetched one step ahead (L2 latency)
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        sq[q] = ld_global_v4_hint(reinterpret_cast<const uint4 *>(ring_s2(0, L - 1)) + (size_t)((col0 >> 3) + q) * 128 + row,
+                                  pol_stream);
       for (int s = 0; s < 2; ++s) {
         const float u_row = sU[s * 4 + (row >> 5)];
         for (int l = L - 1; l >= 0; --l) {
           const bool top = (l == L - 1);
-          const uint4 *s2src = reinterpret_cast<const uint4 *>(ring_s2(s, l));
-          uint4 sq[4];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) sq[q] = ld_global_v4_hint(s2src + (size_t)((col0 >> 3) + q) * 128 + row, pol_stream);
           if (!top) {
             PH_MARK(6);
-            mbar_wait(acc_full, accph);
+            mbar_wait_sleep(acc_full, accph);
             PH_MARK(5);
             accph ^= 1;
             tc_fence_after();
@@ -467,10 +467,18 @@ __global__ void __launch_bounds__(FusedLayout<H>::NT, 1) k_fused(FusedParams p) 
           wait_sa();
 #pragma unroll
           for (int q = 0; q < 4; ++q)
-            st_shared_v4(a_base + sw128_offset(row, col0 + 8 * q, 128), dp[4 * q], dp[4 * q + 1], dp[4 * q + 2], dp[4 * q + 3]);
+            st_shared_v4(a_base + aoff[q], dp[4 * q], dp[4 * q + 1], dp[4 * q + 2], dp[4 * q + 3]);
           fence_proxy_async_smem();
           mbar_arrive(a_full);
           PH_MARK(4);
+          {  // prefetch s2 of the next backward step
+            const int ns = l > 0 ? s : s + 1, nl = l > 0 ? l - 1 : L - 1;
+            if (ns < 2) {
+              const uint4 *src = reinterpret_cast<const uint4 *>(ring_s2(ns, nl));
+#pragma unroll
+              for (int q = 0; q < 4; ++q) sq[q] = ld_global_v4_hint(src + (size_t)((col0 >> 3) + q) * 128 + row, pol_stream);
+            }
+          }
           if (l >= nu) {  // db of a fused layer: column sums of delta over the warp's 32 rows
             float d[32];
 #pragma unroll
@@ -494,7 +502,7 @@ __global__ void __launch_bounds__(FusedLayout<H>::NT, 1) k_fused(FusedParams p) 
           }
         }
         // the l = 0 step (dW MMA or delta_0 store) must retire before sA is rewritten
-        mbar_wait(acc_full, accph);
+        mbar_wait_sleep(acc_full, accph);
         PH_MARK(5);
         accph ^= 1;
         tc_fence_after();

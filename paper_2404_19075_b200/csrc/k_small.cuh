@@ -134,6 +134,35 @@ __global__ void k_assemble(int H, int L, int64_t P, int nmb, int ksplit, const f
   grad[q] = accumulate ? grad[q] + v : v;
 }
 
+// N1: fused Adam step + re-pack of the bf16 weight images (one thread per parameter).
+__global__ void k_adam_pack(float *__restrict__ params, const float *__restrict__ grad, float *__restrict__ m,
+                            float *__restrict__ v, int64_t P, int H, int L, float lr, float b1, float b2, float eps,
+                            float c1, float c2, float *__restrict__ ctx_params, uint16_t *__restrict__ wpack,
+                            uint16_t *__restrict__ wpack_half) {
+  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= P) return;
+  const float g = grad[q];
+  const float mq = b1 * m[q] + (1.f - b1) * g;
+  const float vq = b2 * v[q] + (1.f - b2) * g * g;
+  m[q] = mq;
+  v[q] = vq;
+  const float w = params[q] - lr * (mq / c1) / (sqrtf(vq / c2) + eps);
+  params[q] = w;
+  ctx_params[q] = w;
+  const int64_t per = (int64_t)H * H + H;
+  if (q < (int64_t)L * per) {
+    const int l = (int)(q / per);
+    const int64_t e = q - (int64_t)l * per;
+    if (e < (int64_t)H * H) {
+      const int o = (int)(e / H), i = (int)(e % H);
+      const uint32_t off = sw128_offset((uint32_t)o, (uint32_t)i, (uint32_t)H) >> 1;
+      __nv_bfloat16 b = __float2bfloat16_rn(w), bh = __float2bfloat16_rn(0.5f * w);
+      wpack[(int64_t)l * H * H + off] = *reinterpret_cast<uint16_t *>(&b);
+      wpack_half[(int64_t)l * H * H + off] = *reinterpret_cast<uint16_t *>(&bh);
+    }
+  }
+}
+
 // Assembly for the fused path (H <= 128): layers [0, nu) from the dW GEMM partials
 // ([l][ks5][128][H]), layers [nu, L) from the fused kernel's per-CTA TMEM partials
 // ([l - nu][ksf][128][H]); fixed summation order -> deterministic.

@@ -41,6 +41,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
   while (!mbar_try_wait(bar, parity)) {
   }
 }
+// Same, but the waiting thread is suspended in hardware (up to ~suspend_ns per attempt)
+// instead of re-issuing the probe: frees issue slots for the warps that have work.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity, uint32_t suspend_ns = 20000) {
+  uint32_t ok;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(suspend_ns)
+        : "memory");
+  } while (!ok);
+}
 
 // ------------------------------------------------------------------ bulk async copies
 // global -> shared, completion signalled on `bar` as transaction bytes.

@@ -229,3 +229,28 @@ def test_full_size_batch_sampled(ctx, dev, O, name):
     rf, _, _ = O.project(g, th, t, f, B, prm, idx[pick])
     assert rel_linf(fhat.cpu().numpy()[pick], rf) <= 2e-3
     assert np.all(np.isfinite(fhat.cpu().numpy()))
+
+
+def test_adam_step_parity_and_repack(ctx, dev, O):
+    """N1: the fused Adam + re-pack kernel matches the oracle's Adam (fp32 tolerance) and the
+    re-packed bf16 images equal those of dinr_set_field_weights on the updated parameters."""
+    g, th, t, f, B, prm = setup_case(ctx, dev, "fan512", {}, {}, "bf16", "beer")
+    P = synth.param_count(f["C"], f["L"])
+    rng = np.random.default_rng(12)
+    grad = rng.standard_normal(P + 1).astype(np.float32) * 1e-3
+    m0 = rng.standard_normal(P).astype(np.float32) * 1e-4
+    v0 = np.abs(rng.standard_normal(P)).astype(np.float32) * 1e-6
+    pt, mt, vt = (torch.tensor(a, device=dev) for a in (prm, m0, v0))
+    D.adam_step(ctx, pt, torch.tensor(grad, device=dev), mt, vt, lr=1e-3, step=3)
+    rp, rm, rv = O.adam_step(prm, grad[:P], m0, v0, lr=1e-3, step=3)
+    assert np.allclose(pt.cpu().numpy(), rp, rtol=1e-5, atol=1e-7)
+    # fp32 arithmetic on |m| ~ 1e-4, |v| ~ 1e-6: absolute rounding ~ 1e-11 / 1e-13 near cancellation
+    assert np.allclose(mt.cpu().numpy(), rm, rtol=1e-5, atol=1e-10)
+    assert np.allclose(vt.cpu().numpy(), rv, rtol=1e-5, atol=1e-12)
+    idx = torch.tensor(synth.pixel_batch("fan512", 200, seed=5), device=dev)
+    f1 = torch.zeros(200, device=dev)
+    D.project(ctx, idx, f1)
+    D.set_field_weights(ctx, f, torch.tensor(B, device=dev), pt.clone())
+    f2 = torch.zeros(200, device=dev)
+    D.project(ctx, idx, f2)
+    assert torch.equal(f1, f2)
