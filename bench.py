@@ -239,8 +239,14 @@ def main():
     pool = 4
     idx_pool = [torch.tensor(pdist.shard_batch(name, n, rank, world, seed=1000 + 17 * q), device=dev)
                 for q in range(pool)]
-    y_pool = [torch.tensor(synth.synthetic_y(n, 2.0 * synth.WORKLOADS[name]["mu0"] * g["fov_radius"], seed=q),
-                           device=dev) for q in range(pool)]
+    # measured data: exact line integrals of the workload phantom + 0.1 % transmission-space noise
+    # (N2), synthesised on the GPU by the library before the timed region
+    y_pool = []
+    for q in range(pool):
+        yq = torch.zeros(n, device=dev)
+        D.phantom_project(ctx, synth.phantom(name), idx_pool[q], yq, combine=args.combine, noise_frac=1e-3, seed=q,
+                          stream=stream)
+        y_pool.append(yq)
     grad = torch.zeros(P + 1, device=dev)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
 

@@ -161,6 +161,27 @@ dinr_status dinr_adam_step(dinr_ctx *ctx, float *params_dev, const float *grad_d
                            int64_t count, double lr, double beta1, double beta2, double eps, int64_t step,
                            void *stream);
 
+/* Analytic phantom primitive (NEXT row N2): kind 0 = indicator ellipsoid (value mu), 1 = smooth
+ * ellipsoid mu_c (1 - rho^2)^2, 2 = Gaussian A exp(-rho^2/2) with sigmas = axes.  Axis-aligned in
+ * the object frame, centre(t) = center + velocity t, axes(t) = axes + axes_rate t. */
+typedef struct {
+  int32_t kind;
+  int32_t reserved;
+  double value;
+  double center[3], velocity[3], axes[3], axes_rate[3];
+} dinr_primitive;
+
+/* Measured-data synthesis (N2): exact line integrals of the phantom along every sub-ray of the
+ * n pixels (fp64, closed forms, on the K1 ray records), combined per pixel with `combine`
+ * (dinr_combine) into fhat_dev[n] = -log(I/I0); p_sub_dev[n*S] (or NULL) gets the noiseless
+ * sub-ray integrals.  noise_frac > 0 adds transmission-space Gaussian noise of std
+ * noise_frac*sqrt(T) (eq:forwmod P:261-272, R24) from a counter-based generator keyed by
+ * (seed, pixel index) -- reproducible and independent of launch order.  prims_host: host array
+ * of n_prims (<= 64) primitives, copied before return.  Requires dinr_set_geometry. */
+dinr_status dinr_phantom_project(dinr_ctx *ctx, const dinr_primitive *prims_host, int32_t n_prims,
+                                 const int64_t *idx_dev, int64_t n, int32_t combine, double noise_frac,
+                                 uint64_t seed, float *fhat_dev, float *p_sub_dev, void *stream);
+
 /* fp64 ray records of kernel K1 (geometry / ray setup) for n pixels: rec_dev[n*S*9] =
  * {o.x,o.y,o.z, d.x,d.y,d.z, delta_min, delta_max, chord} per sub-ray, where o is the
  * rotated source, d = rotated detector point - o, [delta_min, delta_max] the FOV bounds

@@ -28,7 +28,7 @@ EXPORTS = [
     "dinr_set_geometry", "dinr_set_field_weights", "dinr_project", "dinr_project_and_grad",
     "dinr_project_and_grad_host", "dinr_ray_records", "dinr_nccl_unique_id", "dinr_comm_init",
     "dinr_allreduce_grads", "dinr_get_device_status", "dinr_set_timing", "dinr_read_timing",
-    "dinr_launch_count", "dinr_adam_step",
+    "dinr_launch_count", "dinr_adam_step", "dinr_phantom_project",
 ]
 
 
@@ -47,6 +47,14 @@ class Geometry(C.Structure):
         ("rot_center_x", C.c_double), ("z_lo", C.c_double), ("z_hi", C.c_double),
         ("t_lo", C.c_double), ("t_hi", C.c_double),
     ]
+
+
+class Primitive(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("reserved", C.c_int32), ("value", C.c_double), ("center", C.c_double * 3),
+                ("velocity", C.c_double * 3), ("axes", C.c_double * 3), ("axes_rate", C.c_double * 3)]
+
+
+PRIM_KINDS = {"indicator": 0, "smooth": 1, "gaussian": 2}
 
 
 class FieldDesc(C.Structure):
@@ -97,6 +105,7 @@ def load(path: str = SO_PATH):
         "dinr_read_timing": (st, [vp, C.c_int, d, C.POINTER(C.c_int64), C.c_int]),
         "dinr_launch_count": (i64, [vp]),
         "dinr_adam_step": (st, [vp, vp, vp, vp, vp, i64, C.c_double, C.c_double, C.c_double, C.c_double, i64, vp]),
+        "dinr_phantom_project": (st, [vp, vp, i32, vp, i64, i32, C.c_double, C.c_uint64, vp, vp, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -185,6 +194,23 @@ def adam_step(ctx, params, grad, m, v, lr, step, beta1=0.9, beta2=0.999, eps=1e-
     """N1: fused Adam update of params (in place) + re-pack of the bf16 weight images."""
     _check(ctx, load().dinr_adam_step(ctx, _ptr(params), _ptr(grad), _ptr(m), _ptr(v), params.numel(), lr, beta1,
                                       beta2, eps, step, _stream(stream, params)))
+
+
+def phantom_project(ctx, prims, idx, fhat, p_sub=None, combine="beer", noise_frac=0.0, seed=0, stream=None):
+    """N2: exact line integrals of an analytic phantom (list of dicts as in synth.phantom), with
+    optional transmission-space noise."""
+    arr = (Primitive * max(1, len(prims)))()
+    for q, pr in enumerate(prims):
+        arr[q].kind = PRIM_KINDS[pr["kind"]]
+        arr[q].value = pr["value"]
+        for k in range(3):
+            arr[q].center[k] = pr["center"][k]
+            arr[q].velocity[k] = pr.get("velocity", (0, 0, 0))[k]
+            arr[q].axes[k] = pr["axes"][k]
+            arr[q].axes_rate[k] = pr.get("axes_rate", (0, 0, 0))[k]
+    _check(ctx, load().dinr_phantom_project(ctx, arr, len(prims), _ptr(idx), idx.numel(), COMBINES[combine],
+                                            float(noise_frac), int(seed), _ptr(fhat), _ptr(p_sub),
+                                            _stream(stream, idx)))
 
 
 def ray_records(ctx, idx, rec, stream=None):

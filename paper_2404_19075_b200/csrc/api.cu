@@ -21,6 +21,7 @@
 #include "k_tc_dw.cuh"
 #include "k_tc_mlp.cuh"
 #include "k_fused.cuh"
+#include "k_phantom.cuh"
 #include "nccl_dl.cuh"
 
 using namespace dinr;
@@ -649,6 +650,7 @@ dinr_status dinr_destroy(dinr_ctx *c) {
   cudaFree(c->d_params);
   cudaFree(c->d_wpack);
   cudaFree(c->d_wpack_half);
+  cudaFree(c->d_prims);
   cudaFree(c->scratch);
   cudaFree(c->d_flags);
   delete c;
@@ -773,6 +775,41 @@ dinr_status dinr_adam_step(dinr_ctx *c, float *params, const float *grad, float 
   k_adam_pack<<<(unsigned)((c->P + 255) / 256), 256, 0, st>>>(params, grad, m, v, c->P, c->H, c->L, (float)lr,
                                                               (float)b1, (float)b2, (float)eps, c1, c2, c->d_params,
                                                               c->d_wpack, c->d_wpack_half);
+  CUDA_TRY(c, cudaGetLastError());
+  return DINR_OK;
+}
+
+dinr_status dinr_phantom_project(dinr_ctx *c, const dinr_primitive *prims, int32_t np, const int64_t *idx, int64_t n,
+                                 int32_t combine, double noise_frac, uint64_t seed, float *fhat, float *p_sub,
+                                 void *stream) {
+  if (!c) return DINR_EINVAL;
+  if (!c->have_geom) return fail(c, DINR_ESTATE, "dinr_set_geometry must be called first");
+  if (np < 0 || np > 64 || (np > 0 && !prims) || n < 0 || (n > 0 && (!idx || !fhat)) ||
+      (combine != DINR_BEER && combine != DINR_LINEAR) || !(noise_frac >= 0))
+    return fail(c, DINR_EINVAL, "bad arguments (0 <= n_prims <= 64, combine, noise_frac >= 0)");
+  std::vector<PrimDev> h((size_t)std::max(1, np));
+  for (int q = 0; q < np; ++q) {
+    if (prims[q].kind < 0 || prims[q].kind > 2) return fail(c, DINR_EINVAL, "primitive kind must be 0, 1 or 2");
+    h[q].kind = prims[q].kind;
+    h[q].value = prims[q].value;
+    for (int k = 0; k < 3; ++k) {
+      if (!(prims[q].axes[k] > 0)) return fail(c, DINR_EINVAL, "primitive axes must be > 0");
+      h[q].c0[k] = prims[q].center[k];
+      h[q].vel[k] = prims[q].velocity[k];
+      h[q].a0[k] = prims[q].axes[k];
+      h[q].arate[k] = prims[q].axes_rate[k];
+    }
+  }
+  if (n == 0) return DINR_OK;
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!c->d_prims) CUDA_TRY(c, cudaMalloc(&c->d_prims, sizeof(PrimDev) * 64));
+  CUDA_TRY(c, cudaMemcpyAsync(c->d_prims, h.data(), sizeof(PrimDev) * np, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(c, cudaStreamSynchronize(st));  // the host staging vector dies with this call
+  Launch L_(c, T_RAYS, st);
+  k_phantom_project<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(geom_params(c), c->d_views, idx, n,
+                                                                (const PrimDev *)c->d_prims, np, combine, noise_frac,
+                                                                seed, fhat, p_sub, c->d_flags);
   CUDA_TRY(c, cudaGetLastError());
   return DINR_OK;
 }

@@ -76,6 +76,7 @@ struct dinr_ctx {
   size_t scratch_cap = 0;
   int *d_flags = nullptr;  // [0] = out-of-range index seen
   float *d_ones = nullptr;
+  void *d_prims = nullptr;  // N2 phantom primitives (64 slots)
 
   // instrumentation
   bool timing = false;

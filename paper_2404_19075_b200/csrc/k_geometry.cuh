@@ -30,30 +30,17 @@ __device__ __forceinline__ void rot_cs(double x, double y, double c, double s, d
   yo = dsub(dadd(dmul(x, s), dmul(y, c)), dmul(xs0, s));
 }
 
-__global__ void k_ray_setup(GeomParams gp, const double *__restrict__ views, const int64_t *__restrict__ idx,
-                            int64_t n, double *__restrict__ rec64, float4 *__restrict__ rec32,
-                            int *__restrict__ flags) {
-  const int S = gp.sub_x * gp.sub_z;
-  int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (gid >= n * S) return;
-  int64_t p = gid / S;
-  int s = (int)(gid - p * S);
+// One sub-ray's fp64 record {o, d, delta_min, delta_max, chord}; returns false for an
+// out-of-range pixel index.  Shared by K1 and the analytic phantom projector (N2).
+__device__ __forceinline__ bool ray_fp64(const GeomParams &gp, const double *__restrict__ views, int64_t i, int s,
+                                         double r[9], double &tk) {
   int u = s % gp.sub_x, v = s / gp.sub_x;
-  int64_t i = idx[p];
   int64_t N = (int64_t)gp.n_rows * gp.n_cols;
-  if (i < 0 || i >= gp.M * N) {
-    atomicOr(flags, 1);
-    if (rec64)
-      for (int q = 0; q < 9; ++q) rec64[gid * 9 + q] = 0.0;
-    if (rec32) {
-      rec32[2 * gid] = make_float4(0.f, 0.f, 0.f, 0.f);
-      rec32[2 * gid + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-    return;
-  }
+  if (i < 0 || i >= gp.M * N) return false;
   int64_t k = i / N, nn = i % N;
   int64_t row = nn / gp.n_cols, col = nn % gp.n_cols;
-  double ck = views[3 * k], sk = views[3 * k + 1], tk = views[3 * k + 2];
+  double ck = views[3 * k], sk = views[3 * k + 1];
+  tk = views[3 * k + 2];
 
   double xd = dadd(-gp.cx, dmul(dadd((double)col, __ddiv_rn(dadd((double)u, 0.5), (double)gp.sub_x)), gp.dx));
   double yd = gp.odd;
@@ -88,20 +75,41 @@ __global__ void k_ray_setup(GeomParams gp, const double *__restrict__ views, con
   double xsk, ysk, xdk, ydk;
   rot_cs(xs, ys, ck, sk, gp.xs0, xsk, ysk);
   rot_cs(xd, yd, ck, sk, gp.xs0, xdk, ydk);
-  double ox = xsk, oy = ysk, oz = zs;
-  double dx = dsub(xdk, xsk), dy = dsub(ydk, ysk), dz = ez;
-  if (rec64) {
-    double *r = rec64 + gid * 9;
-    r[0] = ox;
-    r[1] = oy;
-    r[2] = oz;
-    r[3] = dx;
-    r[4] = dy;
-    r[5] = dz;
-    r[6] = dmin;
-    r[7] = dmax;
-    r[8] = chord;
+  r[0] = xsk;
+  r[1] = ysk;
+  r[2] = zs;
+  r[3] = dsub(xdk, xsk);
+  r[4] = dsub(ydk, ysk);
+  r[5] = ez;
+  r[6] = dmin;
+  r[7] = dmax;
+  r[8] = chord;
+  return true;
+}
+
+__global__ void k_ray_setup(GeomParams gp, const double *__restrict__ views, const int64_t *__restrict__ idx,
+                            int64_t n, double *__restrict__ rec64, float4 *__restrict__ rec32,
+                            int *__restrict__ flags) {
+  const int S = gp.sub_x * gp.sub_z;
+  int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= n * S) return;
+  int64_t p = gid / S;
+  int s = (int)(gid - p * S);
+  double rr[9], tk;
+  if (!ray_fp64(gp, views, idx[p], s, rr, tk)) {
+    atomicOr(flags, 1);
+    if (rec64)
+      for (int q = 0; q < 9; ++q) rec64[gid * 9 + q] = 0.0;
+    if (rec32) {
+      rec32[2 * gid] = make_float4(0.f, 0.f, 0.f, 0.f);
+      rec32[2 * gid + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    return;
   }
+  const double ox = rr[0], oy = rr[1], oz = rr[2], dx = rr[3], dy = rr[4], dz = rr[5];
+  const double dmin = rr[6], dmax = rr[7], chord = rr[8];
+  if (rec64)
+    for (int q = 0; q < 9; ++q) rec64[gid * 9 + q] = rr[q];
   if (rec32) {
     // Normalized entry point and per-sample step (R11); weight chord/N_s (R7).
     double ir = 1.0 / gp.r;
