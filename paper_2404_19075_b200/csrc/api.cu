@@ -21,6 +21,7 @@
 #include "k_tc_dw.cuh"
 #include "k_tc_mlp.cuh"
 #include "k_fused.cuh"
+#include "k_fused2.cuh"
 #include "k_phantom.cuh"
 #include "nccl_dl.cuh"
 
@@ -98,7 +99,7 @@ struct Plan {
   int ksplit_simt;
   int nloss;
   // fused training path (k_fused): nf top layers' dW in TMEM, nu = L - nf through K5
-  bool fused;
+  bool fused, fused2;  // fused2: two concurrent tile streams (k_fused2)
   int nf, nu, grid_f, dw_layers;
   uint8_t *ring;
   float *dwf, *dbf;
@@ -115,6 +116,12 @@ bool use_fused(const dinr_ctx *c) {
   static const bool off = std::getenv("DINR_NO_FUSED") != nullptr;
   const int ns = c->geom.samples_per_ray, sn = c->S * ns;
   return !off && c->field.precision == DINR_BF16 && c->H <= 128 && sn <= 256 && 256 % sn == 0 && (ns & (ns - 1)) == 0;
+}
+
+bool use_fused2(const dinr_ctx *c) {
+  static const bool off = std::getenv("DINR_FUSED_V1") != nullptr;
+  const size_t smem = c->H == 64 ? Fused2Layout<64>::smem_bytes(c->L) : Fused2Layout<128>::smem_bytes(c->L);
+  return !off && smem <= 227 * 1024;
 }
 
 int loss_blocks_for(int64_t n) { return (int)std::max<int64_t>(1, (n + kLossThreads - 1) / kLossThreads); }
@@ -155,12 +162,13 @@ size_t plan_layout(dinr_ctx *c, int64_t n, bool train, bool host_io, Plan &pl, v
     pl.db_part = ar.take<float>((size_t)L * pl.nmb * ks * 128);
   }
   pl.fused = train && use_fused(c);
+  pl.fused2 = pl.fused && use_fused2(c);
   pl.nf = pl.nu = pl.grid_f = 0;
   pl.dw_layers = L;
   pl.ring = nullptr;
   pl.dwf = pl.dbf = nullptr;
   if (pl.fused) {
-    pl.nf = std::min(L, 512 / H - 1);
+    pl.nf = std::min(std::min(L, 4), 512 / H - (pl.fused2 ? 2 : 1));  // <= 4: per-thread db registers
     pl.nu = L - pl.nf;
     pl.dw_layers = pl.nu;
     const int64_t n_groups = (pl.nsamp + 255) / 256;
@@ -350,8 +358,8 @@ dinr_status launch_fused(dinr_ctx *c, const Plan &pl, const float *y, cudaStream
   p.db_part = pl.dbf;
   p.head_part = pl.head_part;
   p.loss_part = pl.loss_part;
-  size_t smem = FusedLayout<H>::smem_bytes(c->L);
-  dinr_status s = set_smem(c, k_fused<H>, smem);
+  const size_t smem = pl.fused2 ? Fused2Layout<H>::smem_bytes(c->L) : FusedLayout<H>::smem_bytes(c->L);
+  dinr_status s = pl.fused2 ? set_smem(c, k_fused2<H>, smem) : set_smem(c, k_fused<H>, smem);
   if (s) return s;
 #ifdef DINR_PHASES
   static unsigned long long *dbg = nullptr;
@@ -361,7 +369,10 @@ dinr_status launch_fused(dinr_ctx *c, const Plan &pl, const float *y, cudaStream
 #endif
   {
     Launch L_(c, T_BWD, st);
-    k_fused<H><<<pl.grid_f, FusedLayout<H>::NT, smem, st>>>(p);
+    if (pl.fused2)
+      k_fused2<H><<<pl.grid_f, Fused2Layout<H>::NT, smem, st>>>(p);
+    else
+      k_fused<H><<<pl.grid_f, FusedLayout<H>::NT, smem, st>>>(p);
   }
   CUDA_TRY(c, cudaGetLastError());
 #ifdef DINR_PHASES

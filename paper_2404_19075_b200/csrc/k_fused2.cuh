@@ -1,0 +1,587 @@
+// k_fused2.cuh -- fused training step, two concurrent tile streams (v3 of the fused path).
+//
+// Same math and the same pixel-group contract as k_fused (256 % (S*N_s) == 0, H <= 128), but
+// the two 128-sample tiles of a group run concurrently on two epilogue warpgroups, so the
+// tensor core computes one tile's layer while the other tile's epilogue runs:
+//   WG s (s = 0, 1; 8 warps, 256 threads) owns tile 2g+s; thread = TMEM lane / sample row r and
+//   the H/2 columns of its column half; warp 16 lane 0 issues every tcgen05.mma / bulk copy,
+//   serving the streams in order (s = 0 then 1) at every layer.
+// TMEM: acc[s] = [s*H, (s+1)*H); dW of the top nf = min(L, 512/H - 2) layers at 2H + j*H.
+// SMEM: W_1..W_{L-1} resident; one buffer XB holds W_0 during the forward phase (only the
+// forward needs W_0: there is no e_{-1}) and the h_l reload for the fused dW MMAs during the
+// backward phase; A_0, A_1 operand tiles.
+// Per-tile state (s2 = 2 swish'(z) of every layer, h of the fused layers) goes through the
+// per-CTA L2 ring (evict_last), h/delta images of the unfused layers to the dW GEMM stash.
+#pragma once
+#include "internal.cuh"
+#include "k_fused.cuh"
+#include "ptx_sm100.cuh"
+
+namespace dinr {
+
+template <int H>
+struct Fused2Layout {
+  static constexpr int EPI = 512;                 // 2 warpgroups x 8 warps
+  static constexpr int NT = EPI + 32;             // + control warp
+  static constexpr uint32_t TILE = H * 256u;      // one 128-row bf16 tile image
+  static constexpr uint32_t A_BYTES = H == 64 ? 2 * TILE : TILE;  // H = 64: zero pad block for M = 128 dW
+  static constexpr uint32_t W_LAYER = H * H * 2u;
+  static constexpr uint32_t XB = TILE > W_LAYER ? TILE : W_LAYER;
+  static constexpr int NF_MAX = 512 / H - 2;
+  static size_t smem_bytes(int L) {
+    return 1024 + 2 * (size_t)A_BYTES + XB + (size_t)(L - 1) * W_LAYER + (size_t)L * H * 4 + (H + 4) * 4 +
+           (H / 2) * 16 + 2 * 4 * (H + 4) * 4 + 2 * 128 * 2 * 4 + 3 * 64 * 4 + 256;
+  }
+};
+
+template <int H>
+__global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p) {
+  using LY = Fused2Layout<H>;
+  constexpr int C = H / 2;
+  constexpr int EPI = LY::EPI;
+  constexpr int NCH = H / 64;  // 32-column chunks per thread (column half of H)
+  constexpr uint32_t TILE = LY::TILE;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // keeps the shared address space
+  const int L = p.L, nf = p.nf, nu = L - nf;  // unfused layers 0..nu-1 go through the dW GEMM
+  uint8_t *sA0 = smem;
+  uint8_t *sXB = sA0 + 2 * LY::A_BYTES;
+  uint8_t *sW = sXB + LY::XB;  // W_1..W_{L-1}
+  float *sBias = reinterpret_cast<float *>(sW + (size_t)(L - 1) * LY::W_LAYER);  // 0.5 * b_l
+  float *sWo = sBias + L * H;                                                    // w_o[H], b_o
+  float *sB = sWo + H + 4;                                                       // C x 4
+  float *sHsum = sB + C * 4;             // [2 tiles][4 row chunks][H + 4]
+  float *sMu = sHsum + 2 * 4 * (H + 4);  // [2 tiles][128 rows][2 halves]
+  float *sU = sMu + 2 * 128 * 2;         // [8] upstream u per 32-sample chunk of the group
+  float *sP = sU + 64;                   // [8] chunk sums of M
+  float *sMisc = sP + 64;                // loss partials
+  uint64_t *bars = reinterpret_cast<uint64_t *>(sMisc + 64);
+  uint64_t *a_full = bars, *acc_full = bars + 2, *sa_free = bars + 4;  // [2] each
+  uint64_t *w_bar = bars + 6, *xb_bar = bars + 7;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 8);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (warp == 0) {
+    tmem_alloc(tmem_slot, 512);
+    tmem_relinquish();
+  }
+  if (tid == EPI) {
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&a_full[s], 256);
+      mbar_init(&acc_full[s], 1);
+      mbar_init(&sa_free[s], 1);
+    }
+    mbar_init(w_bar, 1);
+    mbar_init(xb_bar, 1);
+    fence_mbar_init();
+  }
+  const int64_t per = (int64_t)H * H + H;
+  for (int i = tid; i < L * H; i += LY::NT) sBias[i] = 0.5f * p.params[(i / H) * per + (int64_t)H * H + (i % H)];
+  for (int i = tid; i <= H; i += LY::NT) sWo[i] = p.params[(int64_t)L * per + i];
+  for (int i = tid; i < C * 4; i += LY::NT) sB[i] = p.B[i];
+  if (H == 64)  // zero pad blocks after each A tile (rows 64..127 of the M = 128 dW operand)
+    for (int i = tid; i < (int)(2 * TILE / 16); i += LY::NT) {
+      const int s = i / (TILE / 16), k = i % (TILE / 16);
+      reinterpret_cast<uint4 *>(sA0 + s * LY::A_BYTES + TILE)[k] = make_uint4(0, 0, 0, 0);
+    }
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t a0_base = smem_u32(sA0), xb_base = smem_u32(sXB), w_base = smem_u32(sW);
+  const int64_t n_groups = (p.nsamp + 255) / 256;
+  uint8_t *ring = p.ring + (size_t)blockIdx.x * 2 * (L + nf) * TILE;
+  auto ring_s2 = [&](int slot, int l) { return ring + ((size_t)slot * (L + nf) + l) * TILE; };
+  auto ring_h = [&](int slot, int j) { return ring + ((size_t)slot * (L + nf) + L + j) * TILE; };
+  const uint64_t pol_keep = policy_evict_last(), pol_stream = policy_evict_first();
+
+  if (tid >= EPI) {
+    // ===================================================== MMA issuer / copy engine
+    if (lane == 0) {
+      const uint32_t idf = idesc_bf16(128, H, 0, 0), idb = idesc_bf16(128, H, 0, 1), idw = idesc_bf16(128, H, 1, 1);
+      const uint8_t *wsrc = reinterpret_cast<const uint8_t *>(p.wpack_half);
+      if (L > 1) {
+        const uint32_t rb = (uint32_t)(L - 1) * LY::W_LAYER;
+        mbar_arrive_expect_tx(w_bar, rb);
+        for (uint32_t off = 0; off < rb; off += 32768u)
+          bulk_g2s(sW + off, wsrc + LY::W_LAYER + off, min(32768u, rb - off), w_bar);
+        mbar_wait(w_bar, 0);
+      }
+      uint32_t xph = 0;
+      auto xb_load = [&](const void *src, uint32_t bytes, uint64_t pol) {
+        mbar_arrive_expect_tx(xb_bar, bytes);
+        for (uint32_t off = 0; off < bytes; off += 32768u)
+          bulk_g2s_hint(sXB + off, reinterpret_cast<const uint8_t *>(src) + off, min(32768u, bytes - off), xb_bar, pol);
+      };
+      auto xb_wait = [&]() {
+        mbar_wait(xb_bar, xph);
+        xph ^= 1;
+      };
+      xb_load(wsrc, LY::W_LAYER, pol_keep);  // W_0 for the first group's forward
+      bool xb_is_w0 = true, xb_pending = true;
+      uint32_t aph[2] = {0, 0}, ncommit[2] = {0, 0}, dw_init = 0;
+      auto commit = [&](int s) {
+        umma_commit(&acc_full[s]);
+        ++ncommit[s];
+      };
+      auto wait_commit = [&](int s) { mbar_wait(&acc_full[s], (ncommit[s] - 1) & 1); };
+      for (int64_t gi = blockIdx.x; gi < n_groups; gi += gridDim.x) {
+        const bool more = gi + (int64_t)gridDim.x < n_groups;
+        // ---------------------------------------------------------------- forward
+        for (int l = 0; l < L; ++l) {
+          for (int s = 0; s < 2; ++s) {
+            const int64_t tile = 2 * gi + s;
+            const uint32_t a_base = a0_base + s * LY::A_BYTES;
+            mbar_wait(&a_full[s], aph[s]);
+            aph[s] ^= 1;
+            tc_fence_after();
+            if (l >= nu)
+              bulk_s2g_hint(ring_h(s, l - nu), sA0 + s * LY::A_BYTES, TILE, pol_keep);
+            else
+              bulk_s2g_hint(p.hstash + ((size_t)l * p.n_tiles + tile) * TILE, sA0 + s * LY::A_BYTES, TILE,
+                            pol_stream);
+            bulk_commit();
+            if (l == 0 && xb_pending) {
+              xb_wait();
+              xb_pending = false;
+              tc_fence_after();
+            }
+            const uint32_t wl = l == 0 ? xb_base : w_base + (uint32_t)(l - 1) * LY::W_LAYER;
+#pragma unroll
+            for (int kk = 0; kk < H / 16; ++kk)
+              umma_bf16(tmem + s * H, sdesc_sw128(a_base + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
+                        sdesc_sw128(wl + (kk >> 2) * (H * 128) + (kk & 3) * 32, 16, 1024), idf, kk > 0);
+            commit(s);
+            bulk_wait_read_all();
+            mbar_arrive(&sa_free[s]);
+          }
+        }
+        // XB: W_0 -> h_{L-1}(tile 0) once every forward MMA of the group has retired
+        wait_commit(0);
+        wait_commit(1);
+        xb_is_w0 = false;
+        // ---------------------------------------------------------------- backward
+        // (the loss runs on the epilogue warps in between)
+        bool first_fused = true;
+        for (int l = L - 1; l >= 0; --l) {
+          for (int s = 0; s < 2; ++s) {
+            const int64_t tile = 2 * gi + s;
+            const uint32_t a_base = a0_base + s * LY::A_BYTES;
+            const bool fused = l >= nu;
+            if (fused && first_fused) {
+              xb_load(ring_h(s, l - nu), TILE, pol_stream);
+              first_fused = false;
+            }
+            mbar_wait(&a_full[s], aph[s]);
+            aph[s] ^= 1;
+            tc_fence_after();
+            bool st = false;
+            if (fused) {
+              xb_wait();
+              tc_fence_after();
+              const uint32_t dwt = tmem + (uint32_t)(2 * H + (l - nu) * H);
+              const uint32_t seen = (dw_init >> (l - nu)) & 1u;  // TMEM is not zeroed: first MMA overwrites
+              dw_init |= 1u << (l - nu);
+#pragma unroll
+              for (int kk = 0; kk < 8; ++kk)
+                umma_bf16(dwt, sdesc_sw128(a_base + kk * 2048, 16384, 1024), sdesc_sw128(xb_base + kk * 2048, 16384, 1024),
+                          idw, (seen || kk > 0) ? 1u : 0u);
+            } else {
+              bulk_s2g_hint(p.dstash + ((size_t)l * p.n_tiles + tile) * TILE, sA0 + s * LY::A_BYTES, TILE, pol_stream);
+              bulk_commit();
+              st = true;
+            }
+            if (l > 0) {
+              const uint32_t wl = w_base + (uint32_t)(l - 1) * LY::W_LAYER;
+#pragma unroll
+              for (int kk = 0; kk < H / 16; ++kk)
+                umma_bf16(tmem + s * H, sdesc_sw128(a_base + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
+                          sdesc_sw128(wl + kk * 2048, H * 128, 1024), idb, kk > 0);
+            }
+            commit(s);
+            if (st) bulk_wait_read_all();
+            mbar_arrive(&sa_free[s]);
+            if (fused) {
+              // XB is reused: wait until this dW MMA has retired, then load the next operand
+              wait_commit(s);
+              const int ns = s == 0 ? 1 : 0, nl = s == 0 ? l : l - 1;
+              if (nl >= nu) {
+                xb_load(ring_h(ns, nl - nu), TILE, pol_stream);
+              } else if (more) {
+                xb_load(wsrc, LY::W_LAYER, pol_keep);  // W_0 for the next group's forward
+                xb_is_w0 = true;
+                xb_pending = true;
+              }
+            }
+          }
+        }
+      }
+      (void)xb_is_w0;
+      if (xb_pending) xb_wait();
+      bulk_wait_all();
+    }
+    __syncwarp();
+  } else {
+    // ===================================================== epilogue warpgroups
+    const int s = tid >> 8;                  // stream / tile slot of the group
+    const int wt = tid & 255;
+    const int row = wt & 127, ch = wt >> 7;  // sample row, column half
+    const uint32_t a_base = a0_base + s * LY::A_BYTES;
+    uint32_t aoff[NCH][4];
+#pragma unroll
+    for (int c = 0; c < NCH; ++c)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) aoff[c][q] = sw128_offset(row, ch * (H / 2) + c * 32 + 8 * q, 128);
+    const uint32_t trow = tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(s * H + ch * (H / 2));
+    uint32_t accph = 0, sfph = 0;
+    bool sf_first = true;
+    auto wait_sa = [&]() {
+      if (!sf_first) {
+        mbar_wait_sleep(&sa_free[s], sfph);
+        sfph ^= 1;
+      }
+      sf_first = false;
+    };
+    float dbacc[4][NCH];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) dbacc[j][c] = 0.f;
+    float wo_acc[NCH];
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) wo_acc[c] = 0.f;
+    float bo_acc = 0.f, loss_acc = 0.f;
+    const int rays_per_group = 256 / p.n_s;
+    const int pix_per_group = rays_per_group / p.S;
+    const int chunks_per_ray = p.n_s / 32;
+
+    for (int64_t gi = blockIdx.x; gi < n_groups; gi += gridDim.x) {
+      const int64_t tile = 2 * gi + s;
+      const int64_t g = tile * 128 + row;
+      const bool valid = g < p.nsamp;
+      // ------------------------------------------------------------ a5/a6 features
+      {
+        float rb0 = 0.f, rb1 = 0.f, rb2 = 0.f, rb3 = 0.f;
+        if (valid) {
+          const int64_t ray = g >> p.lg_ns;
+          const float jj = (float)(g & (p.n_s - 1)) + 0.5f;
+          const float4 ra = p.rec32[2 * ray], rv = p.rec32[2 * ray + 1];
+          rb0 = ra.w;
+          rb1 = ra.z + jj * rv.z;
+          rb2 = ra.y + jj * rv.y;
+          rb3 = ra.x + jj * rv.x;
+        }
+        constexpr int NFC = (C / 2) / 8;  // 8-frequency chunks of this thread's half of the frequencies
+        uint32_t pc[NFC][4], ps[NFC][4];
+#pragma unroll
+        for (int fc = 0; fc < NFC; ++fc) {
+          const int c0 = ch * (C / 2) + 8 * fc;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            float cs[2], sn[2];
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const float4 bb = reinterpret_cast<const float4 *>(sB)[c0 + 2 * q + e];
+              const float phi = bb.x * rb0 + bb.y * rb1 + bb.z * rb2 + bb.w * rb3;
+              const float fr = phi - rintf(phi);
+              __sincosf(6.283185307179586f * fr, &sn[e], &cs[e]);
+            }
+            pc[fc][q] = pack_bf16x2(cs[0], cs[1]);
+            ps[fc][q] = pack_bf16x2(sn[0], sn[1]);
+          }
+        }
+        wait_sa();
+#pragma unroll
+        for (int fc = 0; fc < NFC; ++fc) {
+          const int c0 = ch * (C / 2) + 8 * fc;
+          st_shared_v4(a_base + sw128_offset(row, c0, 128), pc[fc][0], pc[fc][1], pc[fc][2], pc[fc][3]);
+          st_shared_v4(a_base + sw128_offset(row, C + c0, 128), ps[fc][0], ps[fc][1], ps[fc][2], ps[fc][3]);
+        }
+      }
+      fence_proxy_async_smem();
+      mbar_arrive(&a_full[s]);
+      // ------------------------------------------------------------ a7/a8 forward layers
+      float mu_part = 0.f;
+      for (int l = 0; l < L; ++l) {
+        const bool last = (l == L - 1);
+        mbar_wait_sleep(&acc_full[s], accph);
+        accph ^= 1;
+        tc_fence_after();
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) {
+          const int col0 = ch * (H / 2) + c * 32;
+          uint32_t hpk[16], s2k[16];
+#pragma unroll
+          for (int hf = 0; hf < 2; ++hf) {
+            uint32_t v[16];
+            tmem_ld16(trow + c * 32 + hf * 16, v);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 16; i += 4) {
+              const float4 b4 = *reinterpret_cast<const float4 *>(sBias + l * H + col0 + hf * 16 + i);
+#pragma unroll
+              for (int e = 0; e < 2; ++e) {
+                const float bb0 = e ? b4.z : b4.x, bb1 = e ? b4.w : b4.y;
+                const uint32_t yb = pack_bf16x2(__uint_as_float(v[i + 2 * e]) + bb0, __uint_as_float(v[i + 2 * e + 1]) + bb1);
+                const uint32_t t = bf2_tanh(yb);
+                hpk[(hf * 16 + i) / 2 + e] = bf2_fma(yb, t, yb);
+                const uint32_t w = bf2_fma(t, t ^ kBf2Sign, kBf2One);
+                s2k[(hf * 16 + i) / 2 + e] = bf2_fma(yb, w, bf2_add(t, kBf2One));
+              }
+            }
+          }
+          uint4 *s2dst = reinterpret_cast<uint4 *>(ring_s2(s, l));
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            st_global_v4_hint(s2dst + (size_t)((col0 >> 3) + q) * 128 + row,
+                              make_uint4(s2k[4 * q], s2k[4 * q + 1], s2k[4 * q + 2], s2k[4 * q + 3]), pol_keep);
+          if (!last) {
+            if (c == 0) wait_sa();
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              st_shared_v4(a_base + aoff[c][q], hpk[4 * q], hpk[4 * q + 1], hpk[4 * q + 2], hpk[4 * q + 3]);
+          } else {
+            float hv[32];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              hv[2 * i] = bf16lo(hpk[i]);
+              hv[2 * i + 1] = bf16hi(hpk[i]);
+            }
+#pragma unroll
+            for (int i = 0; i < 32; ++i) mu_part = fmaf(sWo[col0 + i], hv[i], mu_part);
+#pragma unroll
+            for (int o = 16; o >= 1; o >>= 1) {
+              const bool up = (lane & o) != 0;
+#pragma unroll
+              for (int i = 0; i < o; ++i) {
+                float send = up ? hv[i] : hv[i + o];
+                float keep = up ? hv[i + o] : hv[i];
+                hv[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+              }
+            }
+            sHsum[(s * 4 + (warp & 3)) * (H + 4) + col0 + lane] = valid ? hv[0] : 0.f;
+          }
+        }
+        tc_fence_before();
+        if (!last) {
+          fence_proxy_async_smem();
+          mbar_arrive(&a_full[s]);
+        }
+      }
+      sMu[(s * 128 + row) * 2 + ch] = valid ? mu_part : 0.f;
+      // ------------------------------------------------------------ a9-a11: combine + loss
+      fence_proxy_async_global();
+      named_sync(1, EPI);
+      if (warp < 8) {  // chunk sums of M = mu0 (w_o . h_L + b_o), warp q <-> 32-sample chunk q
+        const int ss = warp >> 2, rr = (warp & 3) * 32 + lane;
+        const float m = sWo[H] + sMu[(ss * 128 + rr) * 2] + sMu[(ss * 128 + rr) * 2 + 1];
+        float a = ((2 * gi + ss) * 128 + rr < p.nsamp) ? p.mu0 * m : 0.f;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+        if (lane == 0) sP[warp] = a;
+      }
+      named_sync(1, EPI);
+      if (tid < pix_per_group) {
+        const int64_t pix = gi * pix_per_group + tid;
+        if (pix < p.n_pix) {
+          float pv[8], wqv[8];
+          for (int ss = 0; ss < p.S; ++ss) {
+            const int ray_l = tid * p.S + ss;
+            const int64_t ray = pix * p.S + ss;
+            wqv[ss] = p.rec32[2 * ray + 1].w;
+            float acc = 0.f;
+            for (int c = 0; c < chunks_per_ray; ++c) acc += sP[ray_l * chunks_per_ray + c];
+            pv[ss] = wqv[ss] > 0.f ? wqv[ss] * acc : 0.f;
+          }
+          float fh, T = 1.f, m = 0.f;
+          if (p.combine == DINR_LINEAR) {
+            float acc = 0.f;
+            for (int ss = 0; ss < p.S; ++ss) acc += pv[ss];
+            fh = acc / (float)p.S;
+          } else {
+            m = pv[0];
+            for (int ss = 1; ss < p.S; ++ss) m = fminf(m, pv[ss]);
+            float acc = 0.f;
+            for (int ss = 0; ss < p.S; ++ss) acc += expf(-(pv[ss] - m));
+            T = acc / (float)p.S;
+            fh = m - logf(T);
+          }
+          if (p.fhat) p.fhat[pix] = fh;
+          const float res = p.y[pix] - fh;
+          loss_acc += res * res;
+          const float gg = -2.f * res * p.inv_n;
+          for (int ss = 0; ss < p.S; ++ss) {
+            const float pi = p.combine == DINR_LINEAR ? 1.f / (float)p.S : expf(-(pv[ss] - m)) / ((float)p.S * T);
+            const float us = gg * pi * wqv[ss] * p.mu0;
+            for (int c = 0; c < chunks_per_ray; ++c) sU[(tid * p.S + ss) * chunks_per_ray + c] = us;
+          }
+        } else {
+          for (int ss = 0; ss < p.S; ++ss)
+            for (int c = 0; c < chunks_per_ray; ++c) sU[(tid * p.S + ss) * chunks_per_ray + c] = 0.f;
+        }
+      }
+      named_sync(1, EPI);
+      // head gradients (warps 0 and 4 of warpgroup 0 own all H columns)
+      if (s == 0 && (warp & 3) == 0) {
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) {
+          const int col = ch * (H / 2) + c * 32 + lane;
+          float a = 0.f;
+#pragma unroll
+          for (int q = 0; q < 8; ++q) a += sU[q] * sHsum[q * (H + 4) + col];
+          wo_acc[c] += a;
+        }
+      }
+      if (tid == 0) {
+        float a = 0.f;
+        for (int q = 0; q < 8; ++q)
+          if (gi * 256 + q * 32 < p.nsamp) a += 32.f * sU[q];
+        bo_acc += a;
+      }
+      // ------------------------------------------------------------ a12 backward
+      const float u_row = sU[s * 4 + (row >> 5)];
+      uint4 sq[NCH][4];
+#pragma unroll
+      for (int c = 0; c < NCH; ++c)
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          sq[c][q] = ld_global_v4_hint(reinterpret_cast<const uint4 *>(ring_s2(s, L - 1)) +
+                                           (size_t)(((ch * (H / 2) + c * 32) >> 3) + q) * 128 + row,
+                                       pol_stream);
+      for (int l = L - 1; l >= 0; --l) {
+        const bool top = (l == L - 1);
+        if (!top) {
+          mbar_wait_sleep(&acc_full[s], accph);
+          accph ^= 1;
+          tc_fence_after();
+        }
+        uint32_t dp[NCH][16];
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) {
+          const int col0 = ch * (H / 2) + c * 32;
+#pragma unroll
+          for (int hf = 0; hf < 2; ++hf) {
+            uint32_t v[16];
+            if (!top) {
+              tmem_ld16(trow + c * 32 + hf * 16, v);
+              tmem_wait_ld();
+            }
+#pragma unroll
+            for (int q2 = 0; q2 < 2; ++q2) {
+              const uint4 w = sq[c][hf * 2 + q2];
+              const uint32_t w4[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const int i = q2 * 8 + 2 * e;
+                const int cc = hf * 16 + i;
+                const float e0 = top ? 0.5f * u_row * sWo[col0 + cc] : __uint_as_float(v[i]);
+                const float e1 = top ? 0.5f * u_row * sWo[col0 + cc + 1] : __uint_as_float(v[i + 1]);
+                dp[c][cc / 2] = bf2_mul(pack_bf16x2(e0, e1), w4[e]);
+              }
+            }
+          }
+        }
+        tc_fence_before();
+        wait_sa();
+#pragma unroll
+        for (int c = 0; c < NCH; ++c)
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            st_shared_v4(a_base + aoff[c][q], dp[c][4 * q], dp[c][4 * q + 1], dp[c][4 * q + 2], dp[c][4 * q + 3]);
+        fence_proxy_async_smem();
+        mbar_arrive(&a_full[s]);
+        if (l > 0) {  // prefetch s2 of the next backward step
+#pragma unroll
+          for (int c = 0; c < NCH; ++c)
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              sq[c][q] = ld_global_v4_hint(reinterpret_cast<const uint4 *>(ring_s2(s, l - 1)) +
+                                               (size_t)(((ch * (H / 2) + c * 32) >> 3) + q) * 128 + row,
+                                           pol_stream);
+        }
+        if (l >= nu) {  // db of a fused layer: column sums of delta over the warp's 32 rows
+#pragma unroll
+          for (int c = 0; c < NCH; ++c) {
+            float d[32];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              d[2 * i] = bf16lo(dp[c][i]);
+              d[2 * i + 1] = bf16hi(dp[c][i]);
+            }
+#pragma unroll
+            for (int o = 16; o >= 1; o >>= 1) {
+              const bool up = (lane & o) != 0;
+#pragma unroll
+              for (int i = 0; i < o; ++i) {
+                float send = up ? d[i] : d[i + o];
+                float keep = up ? d[i + o] : d[i];
+                d[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+              }
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              if (j == l - nu) dbacc[j][c] += d[0];
+          }
+        }
+      }
+      // the l = 0 step (dW MMA or delta_0 store) must retire before A_s is rewritten
+      mbar_wait_sleep(&acc_full[s], accph);
+      accph ^= 1;
+      tc_fence_after();
+    }
+    // ------------------------------------------------------------ flush per-CTA partials
+    named_sync(1, EPI);
+    for (int j = 0; j < nf; ++j) {
+      if (s != (j & 1)) continue;  // warpgroup j%2 flushes fused layer j
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) {
+        const int col0 = ch * (H / 2) + c * 32;
+        uint32_t v[32];
+        tmem_ld32(tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(2 * H + j * H + col0), v);
+        tmem_wait_ld();
+        if (H >= 128 || row < 64) {
+          float *dst = p.dw_part + (((size_t)j * gridDim.x + blockIdx.x) * 128 + row) * H + col0;
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            reinterpret_cast<float4 *>(dst)[q] = make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
+                                                             __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3]));
+        }
+      }
+    }
+    float *red = sHsum;  // reuse: [2 streams][4 row chunks][H + 4]
+    for (int j = 0; j < nf; ++j) {
+      named_sync(1, EPI);
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) red[(s * 4 + (warp & 3)) * (H + 4) + ch * (H / 2) + c * 32 + lane] = dbacc[j][c];
+      named_sync(1, EPI);
+      if (tid < H) {
+        float a = 0.f;
+        for (int w = 0; w < 8; ++w) a += red[w * (H + 4) + tid];
+        p.db_part[((size_t)j * gridDim.x + blockIdx.x) * 128 + tid] = a;
+      }
+    }
+    named_sync(1, EPI);
+    if (s == 0 && (warp & 3) == 0) {
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) p.head_part[(size_t)blockIdx.x * (H + 1) + ch * (H / 2) + c * 32 + lane] = wo_acc[c];
+    }
+    if (tid == 0) p.head_part[(size_t)blockIdx.x * (H + 1) + H] = bo_acc;
+    for (int o = 16; o > 0; o >>= 1) loss_acc += __shfl_xor_sync(0xffffffffu, loss_acc, o);
+    if (lane == 0) sMisc[warp] = loss_acc;
+    named_sync(1, EPI);
+    if (tid == 0) {
+      float a = 0.f;
+      for (int w = 0; w < EPI / 32; ++w) a += sMisc[w];
+      p.loss_part[blockIdx.x] = a;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+}  // namespace dinr
