@@ -49,7 +49,11 @@ def build(force: bool = False, verbose: bool = False, out: str = SO, defines=())
 
 
 if __name__ == "__main__":
-    if "--phases" in sys.argv:  # debug variant with per-phase cycle counters in k_fused
+    if "--variant" in sys.argv:  # experiment variant: python -m ...build --variant tag -DFOO=1 ...
+        tag = sys.argv[sys.argv.index("--variant") + 1]
+        extra = [a[2:] for a in sys.argv if a.startswith("-D")]
+        print(build(force=True, out=os.path.join(HERE, f"libdinr_var_{tag}.so"), defines=extra))
+    elif "--phases" in sys.argv:  # debug variant with per-phase cycle counters in k_fused
         extra = [a[2:] for a in sys.argv if a.startswith("-D")]
         tag = "_".join(e.lower().replace("dinr_exp_", "") for e in extra)
         print(build(force=True, out=os.path.join(HERE, f"libdinr_phases{('_' + tag) if tag else ''}.so"),

@@ -96,6 +96,7 @@ struct Plan {
   int nc;
   int grid_tc;
   int ksplit, nmb;
+  int ks0, ks1;  // dW GEMM K-splits of layer 0 / the other layers (see launch_tc_dw)
   int ksplit_simt;
   int nloss;
   // fused training path (k_fused): nf top layers' dW in TMEM, nu = L - nf through K5
@@ -143,6 +144,7 @@ size_t plan_layout(dinr_ctx *c, int64_t n, bool train, bool host_io, Plan &pl, v
   pl.grid_tc = (int)std::max<int64_t>(1, std::min<int64_t>(pl.n_tiles, (int64_t)c->sm_count * tc_occupancy(c)));
   pl.nmb = c->H == 256 ? 2 : 1;
   pl.ksplit = (int)std::max<int64_t>(1, std::min<int64_t>(pl.n_tiles, (c->sm_count + pl.nmb * c->L - 1) / (pl.nmb * c->L)));
+  pl.ks0 = pl.ks1 = pl.ksplit;
   pl.ksplit_simt = (int)std::max<int64_t>(1, std::min<int64_t>(64, pl.nsamp / 1024));
   pl.nloss = loss_blocks_for(n);
   const int H = c->H, L = c->L;
@@ -173,7 +175,19 @@ size_t plan_layout(dinr_ctx *c, int64_t n, bool train, bool host_io, Plan &pl, v
     pl.dw_layers = pl.nu;
     const int64_t n_groups = (pl.nsamp + 255) / 256;
     pl.grid_f = (int)std::max<int64_t>(1, std::min<int64_t>(n_groups, c->sm_count));
-    pl.ksplit = pl.nu > 0 ? (int)std::max<int64_t>(1, std::min<int64_t>(pl.n_tiles, (c->sm_count + pl.nu - 1) / pl.nu)) : 1;
+    // dW GEMM grid: layer 0 recomputes its input (GRFF features) and gets w0 x the CTAs of a
+    // layer that streams both operands from HBM
+    if (pl.nu > 0) {
+      static const double w0 = std::getenv("DINR_DW_W0") ? std::atof(std::getenv("DINR_DW_W0")) : 2.0;
+      const int sm = c->sm_count;
+      pl.ks0 = pl.nu == 1 ? sm : std::max(1, (int)(sm * w0 / (w0 + pl.nu - 1) + 0.5));
+      pl.ks1 = pl.nu == 1 ? 1 : std::max(1, (sm - pl.ks0) / (pl.nu - 1));
+      pl.ks0 = (int)std::min<int64_t>(pl.ks0, pl.n_tiles);
+      pl.ks1 = (int)std::min<int64_t>(pl.ks1, pl.n_tiles);
+      pl.ksplit = std::max(pl.ks0, pl.nu > 1 ? pl.ks1 : 1);
+    } else {
+      pl.ksplit = 1;
+    }
     pl.ring = ar.take<uint8_t>((size_t)pl.grid_f * 2 * (L + pl.nf) * H * 256);
     pl.dwf = ar.take<float>((size_t)pl.nf * pl.grid_f * 128 * H);
     pl.dbf = ar.take<float>((size_t)pl.nf * pl.grid_f * 128);
@@ -321,11 +335,20 @@ dinr_status launch_tc_dw(dinr_ctx *c, const Plan &pl, cudaStream_t st) {
   p.nmb = pl.nmb;
   p.dw_part = pl.dw_part;
   p.db_part = pl.db_part;
+  p.feat0 = pl.fused ? 1 : 0;  // the fused kernels do not stash layer 0's input
+  p.rec32 = pl.rec32;
+  p.B = c->d_B;
+  p.n_s = c->geom.samples_per_ray;
+  p.lg_ns = 0;
+  while ((1 << p.lg_ns) < p.n_s) ++p.lg_ns;
+  p.nsamp = pl.nsamp;
   size_t smem = DwLayout<H>::smem_bytes();
   dinr_status s = set_smem(c, k_tc_dw<H>, smem);
   if (s) return s;
   Launch L_(c, T_DW, st);
-  k_tc_dw<H><<<dim3(pl.ksplit, pl.nmb, pl.dw_layers), 128, smem, st>>>(p);
+  p.ks0 = pl.ks0;
+  p.ks1 = pl.ks1;
+  k_tc_dw<H><<<dim3(pl.ks0 + (pl.dw_layers - 1) * pl.ks1, pl.nmb, 1), DwLayout<H>::NT, smem, st>>>(p);
   CUDA_TRY(c, cudaGetLastError());
   return DINR_OK;
 }
@@ -376,7 +399,21 @@ dinr_status launch_fused(dinr_ctx *c, const Plan &pl, const float *y, cudaStream
   }
   CUDA_TRY(c, cudaGetLastError());
 #ifdef DINR_PHASES
-  {
+  if (pl.fused2) {
+    std::vector<unsigned long long> h((size_t)pl.grid_f * 32);
+    cudaStreamSynchronize(st);
+    cudaMemcpy(h.data(), dbg, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost);
+    const double groups = (double)((pl.nsamp + 255) / 256);
+    for (int s = 0; s < 2; ++s) {
+      double tot[9] = {0};
+      for (int b = 0; b < pl.grid_f; ++b)
+        for (int k = 0; k < 9; ++k) tot[k] += (double)h[(size_t)b * 32 + s * 16 + k];
+      std::fprintf(stderr, "[dinr phases] stream %d cycles per group: feat %.0f fwd_wait %.0f fwd_epi %.0f loss %.0f "
+                           "bwd_wait %.0f bwd_epi %.0f bwd_db %.0f end_wait %.0f (wait_sa %.0f)\n",
+                   s, tot[0] / groups, tot[1] / groups, tot[2] / groups, tot[3] / groups, tot[4] / groups,
+                   tot[5] / groups, tot[6] / groups, tot[7] / groups, tot[8] / groups);
+    }
+  } else {
     std::vector<unsigned long long> h((size_t)pl.grid_f * 8);
     cudaStreamSynchronize(st);
     cudaMemcpy(h.data(), dbg, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost);

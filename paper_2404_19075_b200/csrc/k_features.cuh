@@ -1,0 +1,45 @@
+// k_features.cuh -- GRFF input encoding of one sample (a5/a6 of the hot path), shared by the
+// fused training kernels and the dW GEMM (which recomputes layer 0's input instead of
+// re-reading it from HBM).  gamma(x) = [cos(2 pi B x), sin(2 pi B x)] (eq:grff)
+// evaluated at the ray-sample coordinates from the fp32 ray records (R6, R9).
+#pragma once
+#include "internal.cuh"
+#include "ptx_sm100.cuh"
+
+namespace dinr {
+
+// (t, z, y, x) coordinates of global sample g = ray * n_s + j, j-th midpoint of the ray
+// (rec32[2 ray] = origin + t, rec32[2 ray + 1] = step + quadrature weight).  Zero if !valid.
+__device__ __forceinline__ float4 grff_coords(const float4 *__restrict__ rec32, int64_t g, int lg_ns, int n_s,
+                                              bool valid) {
+  float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (valid) {
+    const int64_t ray = g >> lg_ns;
+    const float jj = (float)(g & (n_s - 1)) + 0.5f;
+    const float4 ra = rec32[2 * ray], rv = rec32[2 * ray + 1];
+    r.x = ra.w;
+    r.y = ra.z + jj * rv.z;
+    r.z = ra.y + jj * rv.y;
+    r.w = ra.x + jj * rv.x;
+  }
+  return r;
+}
+
+// Frequencies c0 .. c0+7 (B rows as float4 in shared memory): packed bf16 cos / sin pairs.
+__device__ __forceinline__ void grff8(const float4 *sB4, int c0, float4 rb, uint32_t (&pc)[4], uint32_t (&ps)[4]) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    float cs[2], sn[2];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const float4 bb = sB4[c0 + 2 * q + e];
+      const float phi = bb.x * rb.x + bb.y * rb.y + bb.z * rb.z + bb.w * rb.w;
+      const float fr = phi - rintf(phi);  // phase mod 1: keeps __sincosf in its accurate range
+      __sincosf(6.283185307179586f * fr, &sn[e], &cs[e]);
+    }
+    pc[q] = pack_bf16x2(cs[0], cs[1]);
+    ps[q] = pack_bf16x2(sn[0], sn[1]);
+  }
+}
+
+}  // namespace dinr

@@ -16,6 +16,7 @@
 #pragma once
 #include "internal.cuh"
 #include "ptx_sm100.cuh"
+#include "k_features.cuh"
 
 namespace dinr {
 
@@ -148,7 +149,7 @@ __global__ void __launch_bounds__(FusedLayout<H>::NT, 1) k_fused(FusedParams p) 
             // h_l (the A tile) is an operand of dW_l: fused -> L2 ring, unfused -> dW GEMM stash
             if (l >= nu)
               bulk_s2g_hint(ring_h(s, l - nu), sA, TILE, pol_keep);
-            else
+            else if (l > 0)  // layer 0's input (the GRFF features) is recomputed by the dW GEMM
               bulk_s2g_hint(p.hstash + ((size_t)l * p.n_tiles + tile) * TILE, sA, TILE, pol_stream);
             bulk_commit();
             const uint32_t wl = w_base + (uint32_t)l * LY::W_LAYER;
@@ -244,35 +245,11 @@ __global__ void __launch_bounds__(FusedLayout<H>::NT, 1) k_fused(FusedParams p) 
         const int64_t g = tile * 128 + row;
         const bool valid = g < p.nsamp;
         {  // a5/a6: sample point, normalization and GRFF features of this thread's 16 frequencies
-          float rb0 = 0.f, rb1 = 0.f, rb2 = 0.f, rb3 = 0.f;
-          if (valid) {
-            const int64_t ray = g >> p.lg_ns;  // N_s is a power of two on this path
-            float jj = (float)(g & (p.n_s - 1)) + 0.5f;
-            float4 ra = p.rec32[2 * ray], rv = p.rec32[2 * ray + 1];
-            rb0 = ra.w;
-            rb1 = ra.z + jj * rv.z;
-            rb2 = ra.y + jj * rv.y;
-            rb3 = ra.x + jj * rv.x;
-          }
+          const float4 rb = grff_coords(p.rec32, g, p.lg_ns, p.n_s, valid);  // N_s is a power of two here
           constexpr int NCH = (C / CG) / 8;  // 8-frequency chunks per thread
           uint32_t pc[NCH][4], ps[NCH][4];
 #pragma unroll
-          for (int ch = 0; ch < NCH; ++ch) {
-            const int c0 = cg * (C / CG) + 8 * ch;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              float cs[2], sn[2];
-#pragma unroll
-              for (int e = 0; e < 2; ++e) {
-                const float4 bb = reinterpret_cast<const float4 *>(sB)[c0 + 2 * q + e];
-                float phi = bb.x * rb0 + bb.y * rb1 + bb.z * rb2 + bb.w * rb3;
-                float fr = phi - rintf(phi);
-                __sincosf(6.283185307179586f * fr, &sn[e], &cs[e]);
-              }
-              pc[ch][q] = pack_bf16x2(cs[0], cs[1]);
-              ps[ch][q] = pack_bf16x2(sn[0], sn[1]);
-            }
-          }
+          for (int ch = 0; ch < NCH; ++ch) grff8(reinterpret_cast<const float4 *>(sB), cg * (C / CG) + 8 * ch, rb, pc[ch], ps[ch]);
           wait_sa();
 #pragma unroll
           for (int ch = 0; ch < NCH; ++ch) {

@@ -14,10 +14,36 @@
 // per-CTA L2 ring (evict_last), h/delta images of the unfused layers to the dW GEMM stash.
 #pragma once
 #include "internal.cuh"
+#include "k_features.cuh"
 #include "k_fused.cuh"
 #include "ptx_sm100.cuh"
 
 namespace dinr {
+
+#ifndef DINR_F2_SUSPEND_NS
+#define DINR_F2_SUSPEND_NS 20000
+#endif
+// epilogue-side waits: suspended try_wait (0 ns hint = plain spinning probe)
+__device__ __forceinline__ void f2_wait(uint64_t *bar, uint32_t parity) {
+  if (DINR_F2_SUSPEND_NS > 0)
+    mbar_wait_sleep(bar, parity, DINR_F2_SUSPEND_NS);
+  else
+    mbar_wait(bar, parity);
+}
+// operand-tile handoff: one arrival per warp after the warp's generic-proxy smem writes are fenced
+__device__ __forceinline__ void f2_arrive_tile(uint64_t *bar) {
+#ifdef DINR_F2_THREAD_ARRIVE
+  mbar_arrive(bar);
+#else
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) mbar_arrive(bar);
+#endif
+}
+#ifdef DINR_F2_THREAD_ARRIVE
+constexpr int kF2TileArrivals = 256;
+#else
+constexpr int kF2TileArrivals = 8;
+#endif
 
 template <int H>
 struct Fused2Layout {
@@ -28,8 +54,10 @@ struct Fused2Layout {
   static constexpr uint32_t W_LAYER = H * H * 2u;
   static constexpr uint32_t XB = TILE > W_LAYER ? TILE : W_LAYER;
   static constexpr int NF_MAX = 512 / H - 2;
+  static constexpr uint32_t ONES = 128 * 32;  // no-swizzle [128 rows][16] bf16: columns 0, 1 = 1
+  static constexpr uint32_t BIAS_B = H * 32;  // no-swizzle [H rows][16] bf16: hi, lo of b_l / 2
   static size_t smem_bytes(int L) {
-    return 1024 + 2 * (size_t)A_BYTES + XB + (size_t)(L - 1) * W_LAYER + (size_t)L * H * 4 + (H + 4) * 4 +
+    return 1024 + 2 * (size_t)A_BYTES + XB + (size_t)(L - 1) * W_LAYER + ONES + (size_t)L * BIAS_B + (H + 4) * 4 +
            (H / 2) * 16 + 2 * 4 * (H + 4) * 4 + 2 * 128 * 2 * 4 + 3 * 64 * 4 + 256;
   }
 };
@@ -47,8 +75,10 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
   uint8_t *sA0 = smem;
   uint8_t *sXB = sA0 + 2 * LY::A_BYTES;
   uint8_t *sW = sXB + LY::XB;  // W_1..W_{L-1}
-  float *sBias = reinterpret_cast<float *>(sW + (size_t)(L - 1) * LY::W_LAYER);  // 0.5 * b_l
-  float *sWo = sBias + L * H;                                                    // w_o[H], b_o
+  // biases enter the MMA as one extra K = 16 step: [1 1 0 ..] x [hi lo 0 ..]^T = b_l / 2 in fp32
+  uint8_t *sOnes = sW + (size_t)(L - 1) * LY::W_LAYER;
+  uint8_t *sBiasB = sOnes + LY::ONES;
+  float *sWo = reinterpret_cast<float *>(sBiasB + (size_t)L * LY::BIAS_B);  // w_o[H], b_o
   float *sB = sWo + H + 4;                                                       // C x 4
   float *sHsum = sB + C * 4;             // [2 tiles][4 row chunks][H + 4]
   float *sMu = sHsum + 2 * 4 * (H + 4);  // [2 tiles][128 rows][2 halves]
@@ -67,7 +97,7 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
   }
   if (tid == EPI) {
     for (int s = 0; s < 2; ++s) {
-      mbar_init(&a_full[s], 256);
+      mbar_init(&a_full[s], kF2TileArrivals);
       mbar_init(&acc_full[s], 1);
       mbar_init(&sa_free[s], 1);
     }
@@ -76,7 +106,20 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
     fence_mbar_init();
   }
   const int64_t per = (int64_t)H * H + H;
-  for (int i = tid; i < L * H; i += LY::NT) sBias[i] = 0.5f * p.params[(i / H) * per + (int64_t)H * H + (i % H)];
+  for (int i = tid; i < (int)(LY::ONES + L * LY::BIAS_B) / 4; i += LY::NT) reinterpret_cast<uint32_t *>(sOnes)[i] = 0u;
+  __syncthreads();
+  for (int i = tid; i < 128; i += LY::NT) {
+    *reinterpret_cast<__nv_bfloat16 *>(sOnes + nosw16_offset(i, 0)) = __float2bfloat16_rn(1.f);
+    *reinterpret_cast<__nv_bfloat16 *>(sOnes + nosw16_offset(i, 1)) = __float2bfloat16_rn(1.f);
+  }
+  for (int i = tid; i < L * H; i += LY::NT) {
+    const float hb = 0.5f * p.params[(i / H) * per + (int64_t)H * H + (i % H)];
+    const __nv_bfloat16 hi = __float2bfloat16_rn(hb);
+    const __nv_bfloat16 lo = __float2bfloat16_rn(hb - __bfloat162float(hi));
+    uint8_t *bb = sBiasB + (size_t)(i / H) * LY::BIAS_B;
+    *reinterpret_cast<__nv_bfloat16 *>(bb + nosw16_offset(i % H, 0)) = hi;
+    *reinterpret_cast<__nv_bfloat16 *>(bb + nosw16_offset(i % H, 1)) = lo;
+  }
   for (int i = tid; i <= H; i += LY::NT) sWo[i] = p.params[(int64_t)L * per + i];
   for (int i = tid; i < C * 4; i += LY::NT) sB[i] = p.B[i];
   if (H == 64)  // zero pad blocks after each A tile (rows 64..127 of the M = 128 dW operand)
@@ -90,6 +133,7 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t a0_base = smem_u32(sA0), xb_base = smem_u32(sXB), w_base = smem_u32(sW);
+  const uint32_t ones_base = smem_u32(sOnes), biasb_base = smem_u32(sBiasB);
   const int64_t n_groups = (p.nsamp + 255) / 256;
   uint8_t *ring = p.ring + (size_t)blockIdx.x * 2 * (L + nf) * TILE;
   auto ring_s2 = [&](int slot, int l) { return ring + ((size_t)slot * (L + nf) + l) * TILE; };
@@ -138,7 +182,7 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
             tc_fence_after();
             if (l >= nu)
               bulk_s2g_hint(ring_h(s, l - nu), sA0 + s * LY::A_BYTES, TILE, pol_keep);
-            else
+            else if (l > 0)  // layer 0's input (the GRFF features) is recomputed by the dW GEMM
               bulk_s2g_hint(p.hstash + ((size_t)l * p.n_tiles + tile) * TILE, sA0 + s * LY::A_BYTES, TILE,
                             pol_stream);
             bulk_commit();
@@ -148,10 +192,12 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
               tc_fence_after();
             }
             const uint32_t wl = l == 0 ? xb_base : w_base + (uint32_t)(l - 1) * LY::W_LAYER;
+            umma_bf16(tmem + s * H, sdesc_none(ones_base, 128, 256), sdesc_none(biasb_base + l * LY::BIAS_B, 128, 256),
+                      idf, 0u);
 #pragma unroll
             for (int kk = 0; kk < H / 16; ++kk)
               umma_bf16(tmem + s * H, sdesc_sw128(a_base + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
-                        sdesc_sw128(wl + (kk >> 2) * (H * 128) + (kk & 3) * 32, 16, 1024), idf, kk > 0);
+                        sdesc_sw128(wl + (kk >> 2) * (H * 128) + (kk & 3) * 32, 16, 1024), idf, 1u);
             commit(s);
             bulk_wait_read_all();
             mbar_arrive(&sa_free[s]);
@@ -236,10 +282,29 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
     const uint32_t trow = tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(s * H + ch * (H / 2));
     uint32_t accph = 0, sfph = 0;
     bool sf_first = true;
+#ifdef DINR_PHASES
+    unsigned long long ph_acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0}, ph_t = clock64();
+#define PH2(k)                                 \
+  do {                                         \
+    const unsigned long long _n = clock64();   \
+    ph_acc[k] += _n - ph_t;                    \
+    ph_t = _n;                                 \
+  } while (0)
+#else
+#define PH2(k) \
+  do {         \
+  } while (0)
+#endif
     auto wait_sa = [&]() {
       if (!sf_first) {
-        mbar_wait_sleep(&sa_free[s], sfph);
+#ifdef DINR_PHASES
+        const unsigned long long _w = clock64();
+#endif
+        f2_wait(&sa_free[s], sfph);
         sfph ^= 1;
+#ifdef DINR_PHASES
+        ph_acc[8] += clock64() - _w;
+#endif
       }
       sf_first = false;
     };
@@ -262,35 +327,11 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
       const bool valid = g < p.nsamp;
       // ------------------------------------------------------------ a5/a6 features
       {
-        float rb0 = 0.f, rb1 = 0.f, rb2 = 0.f, rb3 = 0.f;
-        if (valid) {
-          const int64_t ray = g >> p.lg_ns;
-          const float jj = (float)(g & (p.n_s - 1)) + 0.5f;
-          const float4 ra = p.rec32[2 * ray], rv = p.rec32[2 * ray + 1];
-          rb0 = ra.w;
-          rb1 = ra.z + jj * rv.z;
-          rb2 = ra.y + jj * rv.y;
-          rb3 = ra.x + jj * rv.x;
-        }
+        const float4 rb = grff_coords(p.rec32, g, p.lg_ns, p.n_s, valid);
         constexpr int NFC = (C / 2) / 8;  // 8-frequency chunks of this thread's half of the frequencies
         uint32_t pc[NFC][4], ps[NFC][4];
 #pragma unroll
-        for (int fc = 0; fc < NFC; ++fc) {
-          const int c0 = ch * (C / 2) + 8 * fc;
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            float cs[2], sn[2];
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const float4 bb = reinterpret_cast<const float4 *>(sB)[c0 + 2 * q + e];
-              const float phi = bb.x * rb0 + bb.y * rb1 + bb.z * rb2 + bb.w * rb3;
-              const float fr = phi - rintf(phi);
-              __sincosf(6.283185307179586f * fr, &sn[e], &cs[e]);
-            }
-            pc[fc][q] = pack_bf16x2(cs[0], cs[1]);
-            ps[fc][q] = pack_bf16x2(sn[0], sn[1]);
-          }
-        }
+        for (int fc = 0; fc < NFC; ++fc) grff8(reinterpret_cast<const float4 *>(sB), ch * (C / 2) + 8 * fc, rb, pc[fc], ps[fc]);
         wait_sa();
 #pragma unroll
         for (int fc = 0; fc < NFC; ++fc) {
@@ -300,58 +341,83 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
         }
       }
       fence_proxy_async_smem();
-      mbar_arrive(&a_full[s]);
+      PH2(0);
+      f2_arrive_tile(&a_full[s]);
       // ------------------------------------------------------------ a7/a8 forward layers
       float mu_part = 0.f;
       for (int l = 0; l < L; ++l) {
         const bool last = (l == L - 1);
-        mbar_wait_sleep(&acc_full[s], accph);
+        f2_wait(&acc_full[s], accph);
         accph ^= 1;
         tc_fence_after();
+        PH2(1);
+        // 16-column steps; the TMEM load of step k+1 is in flight while step k is computed
+        constexpr int NHC = H / 32;  // 16-column steps in this thread's column half
+        uint32_t va[16], vb[16];
+        tmem_ld16(trow, va);
+        tmem_wait_ld();
+        reg_fence(va);
 #pragma unroll
-        for (int c = 0; c < NCH; ++c) {
-          const int col0 = ch * (H / 2) + c * 32;
-          uint32_t hpk[16], s2k[16];
-#pragma unroll
-          for (int hf = 0; hf < 2; ++hf) {
-            uint32_t v[16];
-            tmem_ld16(trow + c * 32 + hf * 16, v);
+        for (int hc = 0; hc < NHC; ++hc) {
+          uint32_t(&cur)[16] = (hc & 1) ? vb : va;
+          uint32_t(&nxt)[16] = (hc & 1) ? va : vb;
+#ifndef DINR_F2_NO_PREFETCH
+          if (hc + 1 < NHC) tmem_ld16(trow + (hc + 1) * 16, nxt);
+#else
+          if (hc > 0) {
+            tmem_ld16(trow + hc * 16, cur);
             tmem_wait_ld();
+            reg_fence(cur);
+          }
+#endif
+          const int col0 = ch * (H / 2) + hc * 16;
+          uint32_t hpk[8], s2k[8];
 #pragma unroll
-            for (int i = 0; i < 16; i += 4) {
-              const float4 b4 = *reinterpret_cast<const float4 *>(sBias + l * H + col0 + hf * 16 + i);
+          for (int i = 0; i < 16; i += 4) {
 #pragma unroll
-              for (int e = 0; e < 2; ++e) {
-                const float bb0 = e ? b4.z : b4.x, bb1 = e ? b4.w : b4.y;
-                const uint32_t yb = pack_bf16x2(__uint_as_float(v[i + 2 * e]) + bb0, __uint_as_float(v[i + 2 * e + 1]) + bb1);
-                const uint32_t t = bf2_tanh(yb);
-                hpk[(hf * 16 + i) / 2 + e] = bf2_fma(yb, t, yb);
-                const uint32_t w = bf2_fma(t, t ^ kBf2Sign, kBf2One);
-                s2k[(hf * 16 + i) / 2 + e] = bf2_fma(yb, w, bf2_add(t, kBf2One));
-              }
+            for (int e = 0; e < 2; ++e) {
+              const uint32_t yb = pack_bf16x2(__uint_as_float(cur[i + 2 * e]), __uint_as_float(cur[i + 2 * e + 1]));
+#ifdef DINR_EXP_NO_TANH
+              const uint32_t t = yb ^ 0x00400040u;
+#else
+              const uint32_t t = bf2_tanh(yb);
+#endif
+              hpk[i / 2 + e] = bf2_fma(yb, t, yb);
+              const uint32_t w = bf2_fma(t, t ^ kBf2Sign, kBf2One);
+              s2k[i / 2 + e] = bf2_fma(yb, w, bf2_add(t, kBf2One));
             }
           }
           uint4 *s2dst = reinterpret_cast<uint4 *>(ring_s2(s, l));
+#ifndef DINR_EXP_NO_S2ST
 #pragma unroll
-          for (int q = 0; q < 4; ++q)
+          for (int q = 0; q < 2; ++q)
+#else
+          for (int q = 0; q < 2 && l == 99; ++q)
+#endif
             st_global_v4_hint(s2dst + (size_t)((col0 >> 3) + q) * 128 + row,
                               make_uint4(s2k[4 * q], s2k[4 * q + 1], s2k[4 * q + 2], s2k[4 * q + 3]), pol_keep);
           if (!last) {
-            if (c == 0) wait_sa();
+            if (hc == 0) wait_sa();
+#ifndef DINR_EXP_NO_STS
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
-              st_shared_v4(a_base + aoff[c][q], hpk[4 * q], hpk[4 * q + 1], hpk[4 * q + 2], hpk[4 * q + 3]);
+            for (int q = 0; q < 2; ++q)
+#else
+            for (int q = 0; q < 2 && l == 99; ++q)
+#endif
+              st_shared_v4(a_base + aoff[hc >> 1][(hc & 1) * 2 + q], hpk[4 * q], hpk[4 * q + 1], hpk[4 * q + 2],
+                           hpk[4 * q + 3]);
           } else {
-            float hv[32];
+            float hv[16];
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
+            for (int i = 0; i < 8; ++i) {
               hv[2 * i] = bf16lo(hpk[i]);
               hv[2 * i + 1] = bf16hi(hpk[i]);
             }
 #pragma unroll
-            for (int i = 0; i < 32; ++i) mu_part = fmaf(sWo[col0 + i], hv[i], mu_part);
+            for (int i = 0; i < 16; ++i) mu_part = fmaf(sWo[col0 + i], hv[i], mu_part);
+            // column sums over the warp's 32 rows: lanes l and l^16 end with column (l & 15)
 #pragma unroll
-            for (int o = 16; o >= 1; o >>= 1) {
+            for (int o = 8; o >= 1; o >>= 1) {
               const bool up = (lane & o) != 0;
 #pragma unroll
               for (int i = 0; i < o; ++i) {
@@ -360,18 +426,25 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
                 hv[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
               }
             }
-            sHsum[(s * 4 + (warp & 3)) * (H + 4) + col0 + lane] = valid ? hv[0] : 0.f;
+            hv[0] += __shfl_xor_sync(0xffffffffu, hv[0], 16);
+            if (lane < 16) sHsum[(s * 4 + (warp & 3)) * (H + 4) + col0 + lane] = hv[0];
           }
+#ifndef DINR_F2_NO_PREFETCH
+          if (hc + 1 < NHC) {
+            tmem_wait_ld();
+            reg_fence(nxt);
+          }
+#endif
         }
         tc_fence_before();
         if (!last) {
           fence_proxy_async_smem();
-          mbar_arrive(&a_full[s]);
+          f2_arrive_tile(&a_full[s]);
         }
+        PH2(2);
       }
       sMu[(s * 128 + row) * 2 + ch] = valid ? mu_part : 0.f;
       // ------------------------------------------------------------ a9-a11: combine + loss
-      fence_proxy_async_global();
       named_sync(1, EPI);
       if (warp < 8) {  // chunk sums of M = mu0 (w_o . h_L + b_o), warp q <-> 32-sample chunk q
         const int ss = warp >> 2, rr = (warp & 3) * 32 + lane;
@@ -441,6 +514,7 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
       }
       // ------------------------------------------------------------ a12 backward
       const float u_row = sU[s * 4 + (row >> 5)];
+      PH2(3);
       uint4 sq[NCH][4];
 #pragma unroll
       for (int c = 0; c < NCH; ++c)
@@ -452,9 +526,10 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
       for (int l = L - 1; l >= 0; --l) {
         const bool top = (l == L - 1);
         if (!top) {
-          mbar_wait_sleep(&acc_full[s], accph);
+          f2_wait(&acc_full[s], accph);
           accph ^= 1;
           tc_fence_after();
+          PH2(4);
         }
         uint32_t dp[NCH][16];
 #pragma unroll
@@ -490,7 +565,8 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
           for (int q = 0; q < 4; ++q)
             st_shared_v4(a_base + aoff[c][q], dp[c][4 * q], dp[c][4 * q + 1], dp[c][4 * q + 2], dp[c][4 * q + 3]);
         fence_proxy_async_smem();
-        mbar_arrive(&a_full[s]);
+        PH2(5);
+        f2_arrive_tile(&a_full[s]);
         if (l > 0) {  // prefetch s2 of the next backward step
 #pragma unroll
           for (int c = 0; c < NCH; ++c)
@@ -524,13 +600,20 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
               if (j == l - nu) dbacc[j][c] += d[0];
           }
         }
+        PH2(6);
       }
       // the l = 0 step (dW MMA or delta_0 store) must retire before A_s is rewritten
-      mbar_wait_sleep(&acc_full[s], accph);
+      f2_wait(&acc_full[s], accph);
       accph ^= 1;
       tc_fence_after();
+      PH2(7);
     }
     // ------------------------------------------------------------ flush per-CTA partials
+#ifdef DINR_PHASES
+    if (wt == 0 && p.dbg)
+      for (int k = 0; k < 9; ++k) p.dbg[(size_t)blockIdx.x * 32 + s * 16 + k] = ph_acc[k];
+#endif
+#undef PH2
     named_sync(1, EPI);
     for (int j = 0; j < nf; ++j) {
       if (s != (j & 1)) continue;  // warpgroup j%2 flushes fused layer j

@@ -10,6 +10,7 @@
 // fp32 partials are reduced over the K-split in fixed order by k_assemble (deterministic).
 #pragma once
 #include "internal.cuh"
+#include "k_features.cuh"
 #include "ptx_sm100.cuh"
 
 namespace dinr {
@@ -17,8 +18,16 @@ namespace dinr {
 struct DwParams {
   const uint8_t *hstash, *dstash;
   int64_t n_tiles;
-  int L, ksplit, nmb;
+  int L, ksplit, nmb;  // ksplit = partial-slot stride (max of ks0, ks1)
+  int ks0, ks1;        // K-splits (CTAs) of layer 0 and of every other layer: grid.x = ks0 + (layers-1) ks1
   float *dw_part, *db_part;
+  // feat0: layer 0's input tile (GRFF features) is recomputed from the ray records instead of
+  // being read from hstash (fused path: N_s a power of two)
+  int feat0;
+  const float4 *rec32;
+  const float *B;
+  int n_s, lg_ns;
+  int64_t nsamp;
 };
 
 template <int H>
@@ -29,40 +38,48 @@ struct DwLayout {
   static constexpr uint32_t STAGE = A_STAGE + B_STAGE;
   static constexpr int NST = H == 64 ? 4 : (H == 128 ? 3 : 2);
   static constexpr uint32_t TMEM_COLS = H == 64 ? 128 : (H == 128 ? 256 : 512);
-  static size_t smem_bytes() { return 1024 + (size_t)NST * STAGE + 2048 + 256; }
+  static constexpr int NT = 320;  // warp 0: copies, warp 1: MMA, warps 2-9: features, warps 2-5: epilogue
+  static size_t smem_bytes() { return 1024 + (size_t)NST * STAGE + 2048 + (H / 2) * 16 + 256; }
 };
 
 template <int H>
-__global__ void __launch_bounds__(128, 1) k_tc_dw(DwParams p) {
+__global__ void __launch_bounds__(DwLayout<H>::NT, 1) k_tc_dw(DwParams p) {
   using LY = DwLayout<H>;
   constexpr int NST = LY::NST;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // keeps the shared address space
   uint8_t *ones = smem + NST * LY::STAGE;
-  uint64_t *full = reinterpret_cast<uint64_t *>(ones + 2048);
+  float4 *sB4 = reinterpret_cast<float4 *>(ones + 2048);
+  uint64_t *full = reinterpret_cast<uint64_t *>(sB4 + H / 2);
   uint64_t *empty = full + NST;
   uint64_t *done = empty + NST;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(done + 1);
 
   const int tid = threadIdx.x, warp = tid >> 5;
-  const int split = blockIdx.x, mb = blockIdx.y, l = blockIdx.z;
+  const int bx = blockIdx.x, mb = blockIdx.y;
+  const int l = bx < p.ks0 ? 0 : 1 + (bx - p.ks0) / p.ks1;
+  const int split = bx < p.ks0 ? bx : (bx - p.ks0) % p.ks1;
+  const int ks = l == 0 ? p.ks0 : p.ks1;
+  const bool feat = p.feat0 && l == 0;
   if (warp == 0) {
     tmem_alloc(tmem_slot, LY::TMEM_COLS);
     tmem_relinquish();
   }
   if (tid == 0) {
     for (int s = 0; s < NST; ++s) {
-      mbar_init(&full[s], 1);
+      mbar_init(&full[s], feat ? 1 + 8 : 1);  // + one arrival per feature warp
       mbar_init(&empty[s], 1);
     }
     mbar_init(done, 1);
     fence_mbar_init();
   }
   // constant operands: all-ones tile (bf16 1.0 = 0x3F80) and, for H = 64, zero pad blocks
-  for (int i = tid; i < 2048 / 4; i += 128) reinterpret_cast<uint32_t *>(ones)[i] = 0x3F803F80u;
+  for (int i = tid; i < 2048 / 4; i += LY::NT) reinterpret_cast<uint32_t *>(ones)[i] = 0x3F803F80u;
+  if (feat)
+    for (int i = tid; i < H / 2; i += LY::NT) sB4[i] = reinterpret_cast<const float4 *>(p.B)[i];
   if (H == 64)
     for (int s = 0; s < NST; ++s)
-      for (int i = tid; i < 16384 / 16; i += 128)
+      for (int i = tid; i < 16384 / 16; i += LY::NT)
         reinterpret_cast<uint4 *>(smem + s * LY::STAGE + 16384)[i] = make_uint4(0, 0, 0, 0);
   fence_proxy_async_smem();
   tc_fence_before();
@@ -72,20 +89,21 @@ __global__ void __launch_bounds__(128, 1) k_tc_dw(DwParams p) {
   const uint32_t tmem_dw = tmem, tmem_db = tmem + H;
 
   int count = 0;
-  for (int64_t t = split; t < p.n_tiles; t += p.ksplit) ++count;
+  for (int64_t t = split; t < p.n_tiles; t += ks) ++count;
 
   if (tid == 0) {
     int it = 0;
-    for (int64_t t = split; t < p.n_tiles; t += p.ksplit, ++it) {
+    for (int64_t t = split; t < p.n_tiles; t += ks, ++it) {
       int st = it % NST;
       if (it >= NST) mbar_wait(&empty[st], ((it / NST) - 1) & 1);
       uint8_t *sa = smem + st * LY::STAGE, *sb = sa + LY::A_STAGE;
-      mbar_arrive_expect_tx(&full[st], LY::A_COPY + LY::B_STAGE);
+      mbar_arrive_expect_tx(&full[st], LY::A_COPY + (feat ? 0u : LY::B_STAGE));
       const uint8_t *dsrc = p.dstash + ((size_t)l * p.n_tiles + t) * (H * 256) + (size_t)mb * 32768;
       const uint8_t *hsrc = p.hstash + ((size_t)l * p.n_tiles + t) * (H * 256);
       bulk_g2s(sa, dsrc, LY::A_COPY, &full[st]);
-      for (uint32_t off = 0; off < LY::B_STAGE; off += 32768u)
-        bulk_g2s(sb + off, hsrc + off, min(32768u, LY::B_STAGE - off), &full[st]);
+      if (!feat)
+        for (uint32_t off = 0; off < LY::B_STAGE; off += 32768u)
+          bulk_g2s(sb + off, hsrc + off, min(32768u, LY::B_STAGE - off), &full[st]);
     }
   } else if (tid == 32) {
     const uint32_t id_dw = idesc_bf16(128, H, 1, 1);
@@ -108,37 +126,70 @@ __global__ void __launch_bounds__(128, 1) k_tc_dw(DwParams p) {
       umma_commit(&empty[st]);
     }
     umma_commit(done);
+  } else if (warp >= 2 && feat) {
+    // B operand of layer 0 = gamma(x) of the tile's 128 samples, same SW128 image the fused
+    // kernel fed to its layer-0 MMA (thread = sample row)
+    const int row = ((warp & 3) << 5) | (tid & 31);
+    const int half = (warp - 2) >> 2;  // frequencies [half C/2, (half + 1) C/2)
+    constexpr int C = H / 2;
+    int it = 0;
+    for (int64_t t = split; t < p.n_tiles; t += ks, ++it) {
+      const int st = it % NST;
+      const int64_t g = t * 128 + row;
+      const float4 rb = grff_coords(p.rec32, g, p.lg_ns, p.n_s, g < p.nsamp);
+      if (it >= NST) mbar_wait(&empty[st], ((it / NST) - 1) & 1);
+      const uint32_t sb = smem_u32(smem + st * LY::STAGE + LY::A_STAGE);
+#pragma unroll
+      for (int c0 = half * (C / 2); c0 < (half + 1) * (C / 2); c0 += 8) {
+        uint32_t pc[4], ps[4];
+        grff8(sB4, c0, rb, pc, ps);
+        st_shared_v4(sb + sw128_offset(row, c0, 128), pc[0], pc[1], pc[2], pc[3]);
+        st_shared_v4(sb + sw128_offset(row, C + c0, 128), ps[0], ps[1], ps[2], ps[3]);
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if ((tid & 31) == 0) mbar_arrive(&full[st]);
+    }
   }
   __syncwarp();
   if (count > 0) {
     mbar_wait(done, 0);
     tc_fence_after();
   }
-  // epilogue: lane o of the accumulator -> fp32 partial row
-  const int o = tid;
-  const uint32_t trow = (uint32_t)(warp * 32) << 16;
-  float *dst = p.dw_part + ((((size_t)l * p.nmb + mb) * p.ksplit + split) * 128 + o) * H;
-  const bool live = (H >= 128) || o < 64;
+  // epilogue (warps 2-5): lane o of the accumulator -> fp32 partial row
+  if (warp >= 2 && warp < 6) {
+    const int o = ((warp & 3) << 5) | (tid & 31);
+    const uint32_t trow = (uint32_t)((warp & 3) * 32) << 16;
+    float *dst = p.dw_part + ((((size_t)l * p.nmb + mb) * p.ksplit + split) * 128 + o) * H;
+    const bool live = (H >= 128) || o < 64;
 #pragma unroll 1
-  for (int cb = 0; cb < H / 32; ++cb) {
-    uint32_t v[32];
-    tmem_ld32(tmem_dw + trow + cb * 32, v);
-    tmem_wait_ld();
-    if (live) {
+    for (int cb = 0; cb < H / 32; ++cb) {
+      uint32_t v[32];
+      tmem_ld32(tmem_dw + trow + cb * 32, v);
+      tmem_wait_ld();
+      if (live) {
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        float4 f = count > 0 ? make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
-                                           __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3]))
-                             : make_float4(0.f, 0.f, 0.f, 0.f);
-        reinterpret_cast<float4 *>(dst + cb * 32)[q] = f;
+        for (int q = 0; q < 8; ++q) {
+          float4 f = count > 0 ? make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
+                                             __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3]))
+                               : make_float4(0.f, 0.f, 0.f, 0.f);
+          reinterpret_cast<float4 *>(dst + cb * 32)[q] = f;
+        }
       }
     }
-  }
-  {
-    uint32_t v[16];
-    tmem_ld16(tmem_db + trow, v);
-    tmem_wait_ld();
-    if (live) p.db_part[(((size_t)l * p.nmb + mb) * p.ksplit + split) * 128 + o] = count > 0 ? __uint_as_float(v[0]) : 0.f;
+    {
+      uint32_t v[16];
+      tmem_ld16(tmem_db + trow, v);
+      tmem_wait_ld();
+      if (live) p.db_part[(((size_t)l * p.nmb + mb) * p.ksplit + split) * 128 + o] = count > 0 ? __uint_as_float(v[0]) : 0.f;
+    }
+    // slots this layer does not use (ks < ksplit) are zero for the fixed-order reduction
+    if (live)
+      for (int s2 = split + ks; s2 < p.ksplit; s2 += ks) {
+        float4 *z = reinterpret_cast<float4 *>(p.dw_part + ((((size_t)l * p.nmb + mb) * p.ksplit + s2) * 128 + o) * H);
+        for (int q = 0; q < H / 4; ++q) z[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+        p.db_part[(((size_t)l * p.nmb + mb) * p.ksplit + s2) * 128 + o] = 0.f;
+      }
   }
   tc_fence_before();
   __syncthreads();

@@ -47,10 +47,6 @@ struct TcLayout {
   }
 };
 
-__device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
-  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
-}
-
 __device__ __forceinline__ float swish_f(float z) { return z * (0.5f + 0.5f * tanh_approx(0.5f * z)); }
 __device__ __forceinline__ float dswish_f(float z) {
   float s = 0.5f + 0.5f * tanh_approx(0.5f * z);

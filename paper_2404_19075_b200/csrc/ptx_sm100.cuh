@@ -114,6 +114,10 @@ __device__ __forceinline__ uint4 ld_global_v4_hint(const void *p, uint64_t pol) 
   return v;
 }
 
+__device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
+
 // Make generic-proxy shared-memory writes visible to the async proxy (tensor core, TMA).
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -177,6 +181,13 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
       : "r"(taddr));
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+// Pins registers written by an earlier tcgen05.ld behind the tcgen05.wait::ld that precedes this
+// call (the compiler does not know the load is asynchronous and could hoist their uses).
+template <int N>
+__device__ __forceinline__ void reg_fence(uint32_t (&v)[N]) {
+#pragma unroll
+  for (int i = 0; i < N; ++i) asm volatile("" : "+r"(v[i]));
+}
 
 // ------------------------------------------------------------------------ descriptors
 // Shared-memory matrix descriptor, SWIZZLE_128B, Blackwell version 1.
@@ -191,6 +202,20 @@ __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr, uint32_t lbo_byt
   d |= (uint64_t)1 << 46;  // version (sm_100)
   d |= (uint64_t)2 << 61;  // SWIZZLE_128B
   return d;
+}
+// Shared-memory matrix descriptor, no swizzle (K-major "interleaved" core matrices of 8 rows x 16 B):
+// lbo = byte stride between core matrices along K, sbo = byte stride between 8-row groups.
+__device__ __forceinline__ uint64_t sdesc_none(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo_bytes >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;  // version (sm_100); layout type 0 = SWIZZLE_NONE
+  return d;
+}
+// Byte offset of element (row, k < 16) in a no-swizzle K-major [rows][16] image (see sdesc_none(., 128, 256)).
+__host__ __device__ __forceinline__ uint32_t nosw16_offset(uint32_t row, uint32_t k) {
+  return ((row >> 3) * 2u + (k >> 3)) * 128u + (row & 7u) * 16u + (k & 7u) * 2u;
 }
 // Instruction descriptor for kind::f16: bf16 x bf16 -> fp32, dense.
 __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, int a_mn_major, int b_mn_major) {
