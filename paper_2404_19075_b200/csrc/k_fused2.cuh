@@ -387,15 +387,17 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
               s2k[i / 2 + e] = bf2_fma(yb, w, bf2_add(t, kBf2One));
             }
           }
-          uint4 *s2dst = reinterpret_cast<uint4 *>(ring_s2(s, l));
-#ifndef DINR_EXP_NO_S2ST
+          if (last) {
+            // top layer: s2 stays on chip, packed into this thread's already-consumed accumulator
+            // columns (acc[s] is idle until the first backward dX MMA)
+            tmem_st8(trow + hc * 8, s2k);
+          } else {
+            uint4 *s2dst = reinterpret_cast<uint4 *>(ring_s2(s, l));
 #pragma unroll
-          for (int q = 0; q < 2; ++q)
-#else
-          for (int q = 0; q < 2 && l == 99; ++q)
-#endif
-            st_global_v4_hint(s2dst + (size_t)((col0 >> 3) + q) * 128 + row,
-                              make_uint4(s2k[4 * q], s2k[4 * q + 1], s2k[4 * q + 2], s2k[4 * q + 3]), pol_keep);
+            for (int q = 0; q < 2; ++q)
+              st_global_v4_hint(s2dst + (size_t)((col0 >> 3) + q) * 128 + row,
+                                make_uint4(s2k[4 * q], s2k[4 * q + 1], s2k[4 * q + 2], s2k[4 * q + 3]), pol_keep);
+          }
           if (!last) {
             if (hc == 0) wait_sa();
 #ifndef DINR_EXP_NO_STS
@@ -436,6 +438,7 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
           }
 #endif
         }
+        if (last) tmem_wait_st();
         tc_fence_before();
         if (!last) {
           fence_proxy_async_smem();
@@ -516,13 +519,15 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
       const float u_row = sU[s * 4 + (row >> 5)];
       PH2(3);
       uint4 sq[NCH][4];
+      tc_fence_after();
 #pragma unroll
-      for (int c = 0; c < NCH; ++c)
+      for (int c = 0; c < NCH; ++c) {  // top-layer s2 from TMEM (stored by the last forward epilogue)
+        uint32_t w[16];
+        tmem_ld16(trow + c * 16, w);
+        tmem_wait_ld();
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
-          sq[c][q] = ld_global_v4_hint(reinterpret_cast<const uint4 *>(ring_s2(s, L - 1)) +
-                                           (size_t)(((ch * (H / 2) + c * 32) >> 3) + q) * 128 + row,
-                                       pol_stream);
+        for (int q = 0; q < 4; ++q) sq[c][q] = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+      }
       for (int l = L - 1; l >= 0; --l) {
         const bool top = (l == L - 1);
         if (!top) {
