@@ -18,6 +18,55 @@
 
 static const double kPi = 3.14159265358979323846;
 
+/* N3: Philox4x32-10, as defined by Salmon, Moraes, Dror, Shaw (SC'11): 10 rounds of
+ *   (c0, c1, c2, c3) <- (hi(M1 c2) ^ c1 ^ k0, lo(M1 c2), hi(M0 c0) ^ c3 ^ k1, lo(M0 c0)),
+ *   key bumped by the Weyl constants (W0, W1) after every round. */
+void or_philox4x32(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]) {
+  uint32_t c0 = ctr[0], c1 = ctr[1], c2 = ctr[2], c3 = ctr[3], k0 = key[0], k1 = key[1];
+  for (int r = 0; r < 10; ++r) {
+    uint64_t p0 = (uint64_t)0xD2511F53u * c0, p1 = (uint64_t)0xCD9E8D57u * c2;
+    uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1 ^ k0, n1 = (uint32_t)p1;
+    uint32_t n2 = (uint32_t)(p0 >> 32) ^ c3 ^ k1, n3 = (uint32_t)p0;
+    c0 = n0;
+    c1 = n1;
+    c2 = n2;
+    c3 = n3;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  out[0] = c0;
+  out[1] = c1;
+  out[2] = c2;
+  out[3] = c3;
+}
+
+static double u01(uint32_t x) { return (double)(x >> 8) * (1.0 / 16777216.0); }
+
+/* uniforms of global ray `ray` (= pixel index * S + s): counter word 0 = j for the sample
+ * offsets, 0xFFFFFFFF for the sub-pixel offset pair. */
+static void ray_uniforms(const or_geom *g, int64_t ray, uint32_t w0, uint32_t out[4]) {
+  uint32_t ctr[4] = {w0, (uint32_t)((uint64_t)ray & 0xFFFFFFFFu), (uint32_t)((uint64_t)ray >> 32), g->step};
+  uint32_t key[2] = {(uint32_t)(g->seed & 0xFFFFFFFFu), (uint32_t)(g->seed >> 32)};
+  or_philox4x32(ctr, key, out);
+}
+static double sample_u(const or_geom *g, int64_t ray, int j) {
+  if (!g->sampling) return 0.5; /* R8 midpoint */
+  uint32_t o[4];
+  ray_uniforms(g, ray, (uint32_t)j, o);
+  return u01(o[0]);
+}
+static void subpixel_u(const or_geom *g, int64_t ray, double *ux, double *uz) {
+  if (!g->sampling) {
+    *ux = 0.5;
+    *uz = 0.5;
+    return;
+  }
+  uint32_t o[4];
+  ray_uniforms(g, ray, 0xFFFFFFFFu, o);
+  *ux = u01(o[0]);
+  *uz = u01(o[1]);
+}
+
 int64_t or_param_count(int32_t C, int32_t L) {
   /* L FC layers 2C->2C with bias, head 2C->1 with bias. */
   int64_t H = 2 * (int64_t)C;
@@ -68,10 +117,11 @@ int or_fov_delta_bounds(const double src[2], const double dst[2], double xs0, do
  * R9 fan, R10 parallel), O3 (bounds, theta-invariant P:2812-2818), A5 arc length
  * (P:155-172 read as the Euclidean norm, R1), O4 rotation. */
 static void ray_record(const or_geom *g, double ck, double sk, int64_t row, int64_t col, int u,
-                       int v, double rec[9]) {
-  double xd = -g->cx + ((double)col + ((double)u + 0.5) / (double)g->sub_x) * g->dx;
+                       int v, double ux, double uz, double rec[9]) {
+  /* sub-pixel (u, v) at offset (ux, uz) in its cell: 1/2 = centre (midpoint, R8), N3 jitter */
+  double xd = -g->cx + ((double)col + ((double)u + ux) / (double)g->sub_x) * g->dx;
   double yd = g->odd;
-  double zd = -g->cz + ((double)row + ((double)v + 0.5) / (double)g->sub_z) * g->dz;
+  double zd = -g->cz + ((double)row + ((double)v + uz) / (double)g->sub_z) * g->dz;
   double xs, ys = -g->sod, zs;
   if (g->beam == 2) {        /* cone: point source (0,-SOD,0) */
     xs = 0.0;
@@ -102,6 +152,18 @@ static void ray_record(const or_geom *g, double ck, double sk, int64_t row, int6
   rec[8] = chord;
 }
 
+/* all S sub-rays of pixel i (global index), s = v * sub_x + u */
+static void pixel_rays(const or_geom *g, double ck, double sk, int64_t i, int64_t row, int64_t col, double *rec) {
+  int S = g->sub_x * g->sub_z;
+  for (int v = 0; v < g->sub_z; ++v)
+    for (int u = 0; u < g->sub_x; ++u) {
+      int s = v * g->sub_x + u;
+      double ux, uz;
+      subpixel_u(g, i * S + s, &ux, &uz);
+      ray_record(g, ck, sk, row, col, u, v, ux, uz, rec + s * 9);
+    }
+}
+
 /* a1 (R13): i = mN + n -> view k, detector pixel n = row*n_cols + col. */
 static int decode(const or_geom *g, int64_t M, int64_t i, int64_t *k, int64_t *row, int64_t *col) {
   int64_t N = (int64_t)g->n_rows * g->n_cols;
@@ -111,6 +173,17 @@ static int decode(const or_geom *g, int64_t M, int64_t i, int64_t *k, int64_t *r
   *row = n / g->n_cols;
   *col = n % g->n_cols;
   return 0;
+}
+
+void or_sample_offsets(const or_geom *g, const int64_t *idx, int64_t n, double *u, double *uxz) {
+  int S = g->sub_x * g->sub_z, ns = g->n_s;
+  for (int64_t q = 0; q < n; ++q)
+    for (int s = 0; s < S; ++s) {
+      int64_t ray = idx[q] * S + s;
+      if (u)
+        for (int j = 0; j < ns; ++j) u[(q * S + s) * ns + j] = sample_u(g, ray, j);
+      if (uxz) subpixel_u(g, ray, uxz + (q * S + s) * 2, uxz + (q * S + s) * 2 + 1);
+    }
 }
 
 int or_rays(const or_geom *g, const double *theta, int64_t M, const int64_t *idx, int64_t n,
@@ -126,8 +199,7 @@ int or_rays(const or_geom *g, const double *theta, int64_t M, const int64_t *idx
       continue;
     }
     double ck = cos(theta[k]), sk = sin(theta[k]); /* O1 */
-    for (int v = 0; v < g->sub_z; ++v)
-      for (int u = 0; u < g->sub_x; ++u) ray_record(g, ck, sk, row, col, u, v, out + (v * g->sub_x + u) * 9);
+    pixel_rays(g, ck, sk, idx[p], row, col, out);
   }
   return err;
 }
@@ -278,10 +350,11 @@ static void normalize(const or_geom *g, double x, double y, double z, double t, 
   rb[3] = (x - g->xs0) / g->r;
 }
 
-/* O5: midpoint samples delta_j = dmin + (j + 1/2) (dmax - dmin)/N_s (R8), X_j = o + delta_j d. */
-static void sample_point(const double rec[9], int ns, int j, double X[3]) {
+/* O5: samples delta_j = dmin + (j + u_j) (dmax - dmin)/N_s, X_j = o + delta_j d; u_j = 1/2 is
+ * the midpoint rule (R8), u_j ~ U[0,1) the stratified jitter of N3 (eq:estforwmod). */
+static void sample_point(const double rec[9], int ns, int j, double uj, double X[3]) {
   double step = (rec[7] - rec[6]) / (double)ns;
-  double dj = rec[6] + ((double)j + 0.5) * step;
+  double dj = rec[6] + ((double)j + uj) * step;
   X[0] = rec[0] + dj * rec[3];
   X[1] = rec[1] + dj * rec[4];
   X[2] = rec[2] + dj * rec[5];
@@ -329,15 +402,14 @@ static int pixel_forward(const or_geom *g, const double *theta, const double *t,
     return -1;
   }
   double ck = cos(theta[k]), sk = sin(theta[k]);
-  for (int v = 0; v < g->sub_z; ++v)
-    for (int u = 0; u < g->sub_x; ++u) ray_record(g, ck, sk, row, col, u, v, w->rec + (v * g->sub_x + u) * 9);
+  pixel_rays(g, ck, sk, i, row, col, w->rec);
   for (int s = 0; s < S; ++s) {
     const double *rec = w->rec + s * 9;
     double sum = 0.0;
     if (rec[8] > 0.0) { /* R21: a ray contributes iff its chord is positive */
       for (int j = 0; j < ns; ++j) {
         double X[3], rb[4];
-        sample_point(rec, ns, j, X);
+        sample_point(rec, ns, j, sample_u(g, i * S + s, j), X);
         normalize(g, X[0], X[1], X[2], t[k], rb);
         int64_t sj = (int64_t)s * ns + j;
         double *hs = w->hs + (store ? sj * (int64_t)(L + 1) * H : 0);
@@ -540,14 +612,13 @@ int or_project_analytic(const or_geom *g, const double *theta, const double *t, 
         for (int s = 0; s < S; ++s) p[s] = 0.0;
       } else {
         double ck = cos(theta[k]), sk = sin(theta[k]);
-        for (int v = 0; v < g->sub_z; ++v)
-          for (int u = 0; u < g->sub_x; ++u) ray_record(g, ck, sk, row, col, u, v, rec + (v * g->sub_x + u) * 9);
+        pixel_rays(g, ck, sk, idx[q], row, col, rec);
         for (int s = 0; s < S; ++s) {
           double sum = 0.0;
           if (rec[s * 9 + 8] > 0.0)
             for (int j = 0; j < ns; ++j) {
               double X[3];
-              sample_point(rec + s * 9, ns, j, X);
+              sample_point(rec + s * 9, ns, j, sample_u(g, idx[q] * S + s, j), X);
               sum += phantom_mu(prims, n_prims, X, t[k]);
             }
           p[s] = rec[s * 9 + 8] > 0.0 ? (rec[s * 9 + 8] / (double)ns) * sum : 0.0;
@@ -579,8 +650,7 @@ int or_project_exact(const or_geom *g, const double *theta, const double *t, int
         for (int s = 0; s < S; ++s) p[s] = 0.0;
       } else {
         double ck = cos(theta[k]), sk = sin(theta[k]);
-        for (int v = 0; v < g->sub_z; ++v)
-          for (int u = 0; u < g->sub_x; ++u) ray_record(g, ck, sk, row, col, u, v, rec + (v * g->sub_x + u) * 9);
+        pixel_rays(g, ck, sk, idx[q], row, col, rec);
         for (int s = 0; s < S; ++s) {
           const double *r = rec + s * 9;
           p[s] = r[8] > 0.0 ? or_line_integral_exact(prims, n_prims, r, r + 3, r[6], r[7], t[k]) : 0.0;

@@ -36,6 +36,12 @@ typedef struct {
   double xs0;        /* rotation centre x_s0                          */
   double z_lo, z_hi; /* z normalization range (R11)                              */
   double t_lo, t_hi; /* t normalization range (R11)                              */
+  /* N3 ("randomly sampled coordinates"): 0 = midpoint rule (R8),
+   * 1 = stratified jitter of the sub-pixel position and of each sample in its stratum,
+   * uniforms from Philox4x32-10 keyed by seed, counter (j | 0xFFFFFFFF, ray lo, ray hi, step). */
+  int32_t sampling;
+  uint32_t step;
+  uint64_t seed;
 } or_geom;
 
 /* Field (DINR network) description. */
@@ -73,6 +79,13 @@ int or_fov_delta_bounds(const double src[2], const double dst[2], double xs0, do
 /* Ray records for n pixels: per sub-ray s (s = v*sub_x + u) 9 doubles
  * {o.x,o.y,o.z, d.x,d.y,d.z, delta_min, delta_max, chord}.  Out: rec[n*S*9].
  * Returns 0, or -1 if an index is out of range (its records are zeroed). */
+/* Philox4x32-10 (Salmon et al. 2011), the counter-based generator of N3: out = bijection of ctr
+ * under key.  u01(x) = (x >> 8) 2^-24, exactly representable in fp32 and fp64. */
+void or_philox4x32(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);
+/* N3 stratified sample offsets: u[(q*S + s)*N_s + j] in [0,1) for pixel idx[q] (0.5 when
+ * g->sampling == 0), and the sub-pixel offsets ux, uz of each sub-ray (0.5, 0.5 when off). */
+void or_sample_offsets(const or_geom *g, const int64_t *idx, int64_t n, double *u, double *uxz);
+
 int or_rays(const or_geom *g, const double *theta, int64_t M, const int64_t *idx, int64_t n,
             double *rec);
 

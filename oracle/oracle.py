@@ -41,6 +41,7 @@ class OrGeom(C.Structure):
         ("sod", C.c_double), ("odd", C.c_double), ("dx", C.c_double), ("dz", C.c_double),
         ("cx", C.c_double), ("cz", C.c_double), ("r", C.c_double), ("xs0", C.c_double),
         ("z_lo", C.c_double), ("z_hi", C.c_double), ("t_lo", C.c_double), ("t_hi", C.c_double),
+        ("sampling", C.c_int32), ("step", C.c_uint32), ("seed", C.c_uint64),
     ]
 
 
@@ -77,6 +78,8 @@ def lib():
         _lib.or_project_analytic.argtypes = [C.POINTER(OrGeom), d, d, i64, i32, C.POINTER(OrPrim), i32, pi64, i64, d, d]
         _lib.or_project_exact.argtypes = [C.POINTER(OrGeom), d, d, i64, i32, C.POINTER(OrPrim), i32, pi64, i64, d, d]
         _lib.or_adam_step.argtypes = [d, d, d, d, i64, C.c_double, C.c_double, C.c_double, C.c_double, i64]
+        _lib.or_philox4x32.argtypes = [C.POINTER(C.c_uint32), C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]
+        _lib.or_sample_offsets.argtypes = [C.POINTER(OrGeom), pi64, i64, d, d]
         _lib.or_line_integral_exact.restype = C.c_double
         _lib.or_line_integral_exact.argtypes = [C.POINTER(OrPrim), i32, d, d, C.c_double, C.c_double, C.c_double]
     return _lib
@@ -98,12 +101,17 @@ _BEAM = {"parallel": 0, "fan": 1, "cone": 2}
 _COMBINE = {"beer": 0, "linear": 1}
 
 
+_SAMPLING = {"midpoint": 0, "jitter": 1}
+
+
 def geom_struct(g: dict) -> OrGeom:
     """g: the dict produced by paper_2404_19075_b200.synth (plain numbers)."""
     return OrGeom(
         _BEAM[g["beam"]], g["n_rows"], g["n_cols"], g["sub_x"], g["sub_z"], g["n_s"],
         g["sod"], g["odd"], g["pixel_dx"], g["pixel_dz"], g["offset_cx"], g["offset_cz"],
         g["fov_radius"], g["rot_center_x"], g["z_lo"], g["z_hi"], g["t_lo"], g["t_hi"],
+        _SAMPLING[g.get("sampling", "midpoint")], int(g.get("step", 0)) & 0xFFFFFFFF,
+        int(g.get("seed", 0)) & 0xFFFFFFFFFFFFFFFF,
     )
 
 
@@ -126,6 +134,26 @@ def fov_delta_bounds(src, dst, xs0, r):
     lo, hi = C.c_double(), C.c_double()
     hit = lib().or_fov_delta_bounds(_dp(s), _dp(d), xs0, r, C.byref(lo), C.byref(hi))
     return (lo.value, hi.value) if hit else None
+
+
+def philox4x32(ctr, key):
+    """N3 counter-based generator (Philox4x32-10): 4 x uint32 counter, 2 x uint32 key."""
+    c = (C.c_uint32 * 4)(*[int(x) & 0xFFFFFFFF for x in ctr])
+    k = (C.c_uint32 * 2)(*[int(x) & 0xFFFFFFFF for x in key])
+    o = (C.c_uint32 * 4)()
+    lib().or_philox4x32(c, k, o)
+    return [int(x) for x in o]
+
+
+def sample_offsets(g, idx):
+    """N3 offsets: u[n, S, N_s] of every sample in its stratum and uxz[n, S, 2] of every sub-ray."""
+    idx = _i64(idx)
+    S = g["sub_x"] * g["sub_z"]
+    u = np.zeros((len(idx), S, g["n_s"]))
+    uxz = np.zeros((len(idx), S, 2))
+    gs = geom_struct(g)
+    lib().or_sample_offsets(C.byref(gs), idx.ctypes.data_as(C.POINTER(C.c_int64)), len(idx), _dp(u), _dp(uxz))
+    return u, uxz
 
 
 def rays(g, theta, idx):
