@@ -58,6 +58,12 @@ typedef enum { DINR_BEER = 0, DINR_LINEAR = 1 } dinr_combine;
  * FP32_VERIFY: fp32 CUDA-core MLP with accurate sin/cos/exp (the 1e-5 verification mode). */
 typedef enum { DINR_BF16 = 0, DINR_FP32_VERIFY = 1 } dinr_precision;
 
+/* Sample placement (N3): MIDPOINT = sub-pixel centres and sample j at (j + 1/2)/N_s of the FOV
+ * chord (R8); JITTER = stratified jitter, the sub-ray at a uniform point of its sub-pixel cell
+ * and sample j at (j + u_j)/N_s, uniforms from Philox4x32-10 ("randomly sampled
+ * coordinates", eq:estforwmod). */
+typedef enum { DINR_MIDPOINT = 0, DINR_JITTER = 1 } dinr_sampling;
+
 /* Scanner geometry (all lengths in one unit, e.g. mm; fp64).
  *   Detector pixel (row j, col i) covers x_d in [-C_x + i*dx, -C_x + (i+1)*dx),
  *   z_d in [-C_z + j*dz, -C_z + (j+1)*dz) on the plane y = +odd.
@@ -116,6 +122,14 @@ const char *dinr_status_string(dinr_status s);
  * Host arrays, copied before return (synchronous).  cos/sin of theta are taken on the host. */
 dinr_status dinr_set_geometry(dinr_ctx *ctx, const dinr_geometry *g, const double *theta_rad,
                               const double *t, int64_t M);
+
+/* Sample placement for the following calls (host state, no device work; default MIDPOINT).
+ * JITTER draws every uniform from Philox4x32-10 with key = seed (lo, hi words) and counter
+ * (w0, R lo, R hi, step) for global ray R = pixel index * S + s: w0 = j for sample j's offset
+ * u_j = (x >> 8) 2^-24 of output word x; w0 = 0xFFFFFFFF for the sub-pixel offsets (ux, uz)
+ * from output words x, y.  Results depend only on (seed, step, pixel index), not on the batch.
+ * Error: DINR_EINVAL for an unknown mode. */
+dinr_status dinr_set_sampling(dinr_ctx *ctx, dinr_sampling mode, uint64_t seed, uint32_t step);
 
 /* Field weights: B_dev = GRFF matrix (C x 4 fp32, columns t,z,y,x, frozen, R12);
  * params_dev = P fp32 trainable parameters (D5 layout).  Packs bf16 tensor-core operands on

@@ -28,8 +28,9 @@ EXPORTS = [
     "dinr_set_geometry", "dinr_set_field_weights", "dinr_project", "dinr_project_and_grad",
     "dinr_project_and_grad_host", "dinr_ray_records", "dinr_nccl_unique_id", "dinr_comm_init",
     "dinr_allreduce_grads", "dinr_get_device_status", "dinr_set_timing", "dinr_read_timing",
-    "dinr_launch_count", "dinr_adam_step", "dinr_phantom_project",
+    "dinr_launch_count", "dinr_adam_step", "dinr_phantom_project", "dinr_set_sampling",
 ]
+SAMPLINGS = {"midpoint": 0, "jitter": 1}
 
 
 class DinrError(RuntimeError):
@@ -92,6 +93,7 @@ def load(path: str = SO_PATH):
         "dinr_last_error": (C.c_char_p, [vp]),
         "dinr_status_string": (C.c_char_p, [st]),
         "dinr_set_geometry": (st, [vp, C.POINTER(Geometry), d, d, i64]),
+        "dinr_set_sampling": (st, [vp, C.c_int, C.c_uint64, C.c_uint32]),
         "dinr_set_field_weights": (st, [vp, C.POINTER(FieldDesc), vp, vp, vp]),
         "dinr_project": (st, [vp, vp, i64, vp, vp, vp, vp, vp]),
         "dinr_project_and_grad": (st, [vp, vp, i64, vp, vp, C.c_int, vp]),
@@ -163,6 +165,12 @@ def set_geometry(ctx, g: dict, theta, t):
     gs = geometry_struct(g)
     _check(ctx, load().dinr_set_geometry(ctx, C.byref(gs), th.ctypes.data_as(C.POINTER(C.c_double)),
                                          tt.ctypes.data_as(C.POINTER(C.c_double)), len(th)))
+
+
+def set_sampling(ctx, mode: str = "midpoint", seed: int = 0, step: int = 0):
+    """N3 sample placement for the following calls: "midpoint" (R8) or "jitter" (Philox)."""
+    _check(ctx, load().dinr_set_sampling(ctx, SAMPLINGS[mode], int(seed) & 0xFFFFFFFFFFFFFFFF,
+                                         int(step) & 0xFFFFFFFF))
 
 
 def set_field_weights(ctx, f: dict, B, params, precision: str = "bf16", stream=None):

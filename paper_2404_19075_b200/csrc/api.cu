@@ -106,6 +106,8 @@ struct Plan {
   float *dwf, *dbf;
   // carved pointers
   float4 *rec32;
+  uint2 *rid;   // global ray ids (N3 keys)
+  Jitter jit;   // N3 sample placement handed to the MLP kernels
   float *pchunk, *u, *fhat, *loss_part, *head_part, *dw_part, *db_part, *colsum;
   uint8_t *hstash, *dstash, *zstash;
   float *sh, *sz, *sd;
@@ -149,6 +151,11 @@ size_t plan_layout(dinr_ctx *c, int64_t n, bool train, bool host_io, Plan &pl, v
   pl.nloss = loss_blocks_for(n);
   const int H = c->H, L = c->L;
   pl.rec32 = ar.take<float4>(2 * pl.n_rays + 2);
+  pl.rid = ar.take<uint2>(pl.n_rays + 1);
+  pl.jit.rid = c->sampling == DINR_JITTER ? pl.rid : nullptr;
+  pl.jit.seed_lo = (uint32_t)c->seed;
+  pl.jit.seed_hi = (uint32_t)(c->seed >> 32);
+  pl.jit.step = c->step;
   pl.pchunk = ar.take<float>(pl.nsamp / kChunk + 1);
   pl.u = ar.take<float>(pl.n_rays + 1);
   pl.fhat = ar.take<float>(n + 1);
@@ -258,6 +265,10 @@ GeomParams geom_params(const dinr_ctx *c) {
   gp.tc = 0.5 * (g.t_lo + g.t_hi);
   gp.th = 0.5 * (g.t_hi - g.t_lo);
   gp.M = c->M;
+  gp.jitter = c->sampling == DINR_JITTER;
+  gp.seed_lo = (uint32_t)c->seed;
+  gp.seed_hi = (uint32_t)(c->seed >> 32);
+  gp.step = c->step;
   return gp;
 }
 
@@ -267,12 +278,13 @@ dinr_status set_smem(dinr_ctx *c, K kernel, size_t bytes) {
   return DINR_OK;
 }
 
-dinr_status launch_rays(dinr_ctx *c, const int64_t *idx, int64_t n, double *rec64, float4 *rec32, cudaStream_t st) {
+dinr_status launch_rays(dinr_ctx *c, const int64_t *idx, int64_t n, double *rec64, float4 *rec32, uint2 *rid,
+                        cudaStream_t st) {
   if (n == 0) return DINR_OK;
   int64_t threads = n * c->S;
   Launch L_(c, T_RAYS, st);
   k_ray_setup<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(geom_params(c), c->d_views, idx, n, rec64, rec32,
-                                                                  c->d_flags);
+                                                                  rid, c->d_flags);
   CUDA_TRY(c, cudaGetLastError());
   return DINR_OK;
 }
@@ -292,6 +304,7 @@ FieldDev field_dev(const dinr_ctx *c) {
 template <int H>
 dinr_status launch_tc_mlp(dinr_ctx *c, const Plan &pl, bool train, cudaStream_t st) {
   TcParams p{};
+  p.jit = pl.jit;
   p.rec32 = pl.rec32;
   p.nsamp = pl.nsamp;
   p.n_s = c->geom.samples_per_ray;
@@ -327,6 +340,7 @@ dinr_status launch_tc_mlp(dinr_ctx *c, const Plan &pl, bool train, cudaStream_t 
 template <int H>
 dinr_status launch_tc_dw(dinr_ctx *c, const Plan &pl, cudaStream_t st) {
   DwParams p{};
+  p.jit = pl.jit;
   p.hstash = pl.hstash;
   p.dstash = pl.dstash;
   p.n_tiles = pl.n_tiles;
@@ -356,6 +370,7 @@ dinr_status launch_tc_dw(dinr_ctx *c, const Plan &pl, cudaStream_t st) {
 template <int H>
 dinr_status launch_fused(dinr_ctx *c, const Plan &pl, const float *y, cudaStream_t st) {
   FusedParams p{};
+  p.jit = pl.jit;
   p.rec32 = pl.rec32;
   p.n_pix = pl.n;
   p.nsamp = pl.nsamp;
@@ -463,7 +478,7 @@ dinr_status simt_forward(dinr_ctx *c, const Plan &pl, cudaStream_t st) {
   {
     Launch L_(c, T_FWD, st);
     s_features<<<(unsigned)((ns + 255) / 256), 256, 0, st>>>(pl.rec32, ns, c->geom.samples_per_ray, c->d_B, c->C,
-                                                           pl.sh);
+                                                           pl.sh, pl.jit);
   }
   CUDA_TRY(c, cudaGetLastError());
   const int64_t per = (int64_t)H * H + H;
@@ -590,7 +605,7 @@ dinr_status step_grad(dinr_ctx *c, const int64_t *idx, int64_t n, const float *y
     if (!accumulate) CUDA_TRY(c, cudaMemsetAsync(grad, 0, sizeof(float) * (c->P + 1), st));
     return DINR_OK;
   }
-  s = launch_rays(c, idx, n, nullptr, pl.rec32, st);
+  s = launch_rays(c, idx, n, nullptr, pl.rec32, pl.jit.rid ? pl.rid : nullptr, st);
   if (s) return s;
   if (pl.fused) {
     s = c->H == 64 ? launch_fused<64>(c, pl, y, st) : launch_fused<128>(c, pl, y, st);
@@ -706,6 +721,15 @@ dinr_status dinr_destroy(dinr_ctx *c) {
 }
 
 const char *dinr_last_error(const dinr_ctx *c) { return c ? c->err.c_str() : "null context"; }
+
+dinr_status dinr_set_sampling(dinr_ctx *c, dinr_sampling mode, uint64_t seed, uint32_t step) {
+  if (!c) return DINR_EINVAL;
+  if (mode != DINR_MIDPOINT && mode != DINR_JITTER) return fail(c, DINR_EINVAL, "unknown sampling mode");
+  c->sampling = mode;
+  c->seed = seed;
+  c->step = step;
+  return DINR_OK;
+}
 
 dinr_status dinr_set_geometry(dinr_ctx *c, const dinr_geometry *g, const double *theta, const double *t, int64_t M) {
   if (!c || !g || !theta || !t) return c ? fail(c, DINR_EINVAL, "null argument") : DINR_EINVAL;
@@ -867,7 +891,7 @@ dinr_status dinr_ray_records(dinr_ctx *c, const int64_t *idx, int64_t n, double 
   if (!c->have_geom) return fail(c, DINR_ESTATE, "dinr_set_geometry must be called first");
   if (n < 0 || (n > 0 && (!idx || !rec))) return fail(c, DINR_EINVAL, "bad arguments");
   CUDA_TRY(c, cudaSetDevice(c->device));
-  return launch_rays(c, idx, n, rec, nullptr, (cudaStream_t)stream);
+  return launch_rays(c, idx, n, rec, nullptr, nullptr, (cudaStream_t)stream);
 }
 
 dinr_status dinr_project(dinr_ctx *c, const int64_t *idx, int64_t n, float *fhat, float *p_sub, const float *I0,
@@ -882,7 +906,7 @@ dinr_status dinr_project(dinr_ctx *c, const int64_t *idx, int64_t n, float *fhat
   Plan pl;
   dinr_status s = ensure_plan(c, n, false, false, pl);
   if (s) return s;
-  s = launch_rays(c, idx, n, nullptr, pl.rec32, st);
+  s = launch_rays(c, idx, n, nullptr, pl.rec32, pl.jit.rid ? pl.rid : nullptr, st);
   if (s) return s;
   s = c->field.precision == DINR_FP32_VERIFY ? simt_forward(c, pl, st) : tc_forward(c, pl, false, st);
   if (s) return s;

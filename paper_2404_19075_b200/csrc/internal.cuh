@@ -8,6 +8,7 @@
 #include <vector>
 
 #include "../../include/dinr.h"
+#include "philox.cuh"
 
 namespace dinr {
 
@@ -23,12 +24,15 @@ struct GeomParams {
   double sod, odd, dx, dz, cx, cz, r, xs0;
   double zc, zh, tc, th;  // normalization centres / half widths (R11)
   int64_t M;              // number of views
+  int jitter;             // N3: sub-pixel jitter on (seed, step below)
+  uint32_t seed_lo, seed_hi, step;
 };
 
 // Per-ray packed fp32 record (2 x float4), produced by K1, consumed by the MLP kernels:
 //   a = (xbar, ybar, zbar, tbar) normalized coordinates of the point at delta_min
 //   b = (dxbar, dybar, dzbar, wq) normalized per-sample step and quadrature weight chord/N_s
-// Sample j of the ray sits at a.xyz + (j + 1/2) b.xyz (midpoint rule, R8).
+// Sample j of the ray sits at a.xyz + (j + u_j) b.xyz: u_j = 1/2 (midpoint rule, R8) or the
+// N3 stratified jitter (philox.cuh).
 
 struct FieldDev {
   int C, L, H;
@@ -60,6 +64,10 @@ struct dinr_ctx {
   int64_t M = 0;
   int S = 1;
   double *d_views = nullptr;  // M x 3 {cos theta, sin theta, t}
+  // N3 sample placement (dinr_set_sampling)
+  int sampling = DINR_MIDPOINT;
+  uint64_t seed = 0;
+  uint32_t step = 0;
 
   bool have_field = false;
   dinr_field_desc field{};

@@ -8,14 +8,15 @@
 
 namespace dinr {
 
-// (t, z, y, x) coordinates of global sample g = ray * n_s + j, j-th midpoint of the ray
+// (t, z, y, x) coordinates of global sample g = ray * n_s + j, sample j of the ray in its stratum
 // (rec32[2 ray] = origin + t, rec32[2 ray + 1] = step + quadrature weight).  Zero if !valid.
 __device__ __forceinline__ float4 grff_coords(const float4 *__restrict__ rec32, int64_t g, int lg_ns, int n_s,
-                                              bool valid) {
+                                              bool valid, const Jitter &jt) {
   float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
   if (valid) {
     const int64_t ray = g >> lg_ns;
-    const float jj = (float)(g & (n_s - 1)) + 0.5f;
+    const uint32_t j = (uint32_t)(g & (n_s - 1));
+    const float jj = (float)j + sample_offset(jt, ray, j);  // midpoint (R8) or N3 jitter
     const float4 ra = rec32[2 * ray], rv = rec32[2 * ray + 1];
     r.x = ra.w;
     r.y = ra.z + jj * rv.z;

@@ -38,6 +38,7 @@ struct FusedParams {
   float *db_part;         // [nf][grid][128]
   float *head_part;       // [grid][H+1]
   float *loss_part;       // [grid]
+  Jitter jit;                // N3 sample placement
   unsigned long long *dbg;  // DINR_PHASES builds: [grid][8] cycle counters
 };
 
@@ -245,7 +246,7 @@ __global__ void __launch_bounds__(FusedLayout<H>::NT, 1) k_fused(FusedParams p) 
         const int64_t g = tile * 128 + row;
         const bool valid = g < p.nsamp;
         {  // a5/a6: sample point, normalization and GRFF features of this thread's 16 frequencies
-          const float4 rb = grff_coords(p.rec32, g, p.lg_ns, p.n_s, valid);  // N_s is a power of two here
+          const float4 rb = grff_coords(p.rec32, g, p.lg_ns, p.n_s, valid, p.jit);  // N_s is a power of two here
           constexpr int NCH = (C / CG) / 8;  // 8-frequency chunks per thread
           uint32_t pc[NCH][4], ps[NCH][4];
 #pragma unroll

@@ -327,7 +327,7 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
       const bool valid = g < p.nsamp;
       // ------------------------------------------------------------ a5/a6 features
       {
-        const float4 rb = grff_coords(p.rec32, g, p.lg_ns, p.n_s, valid);
+        const float4 rb = grff_coords(p.rec32, g, p.lg_ns, p.n_s, valid, p.jit);
         constexpr int NFC = (C / 2) / 8;  // 8-frequency chunks of this thread's half of the frequencies
         uint32_t pc[NFC][4], ps[NFC][4];
 #pragma unroll

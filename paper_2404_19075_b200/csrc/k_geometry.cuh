@@ -5,8 +5,9 @@
 // one written in DESIGN.md "Ray geometry" (the oracle writes the same formulas in plain C
 // compiled with -ffp-contract=off; cos/sin come from the host libm via the view table):
 //   a1 decode    i = m N + n, row = n / n_cols, col = n % n_cols        (R13)
-//   a3 endpoints x_d = -C_x + (col + (u+1/2)/D_x) dx, y_d = odd,
-//                z_d = -C_z + (row + (v+1/2)/D_z) dz
+//   a3 endpoints x_d = -C_x + (col + (u+ux)/D_x) dx, y_d = odd,
+//                z_d = -C_z + (row + (v+uz)/D_z) dz
+//                ux = uz = 1/2 (midpoint, R8) or the N3 Philox jitter (philox.cuh)
 //                source cone (0,-sod,0) / fan (0,-sod,z_d) / parallel (x_d,-sod,z_d)
 //                                                                        (R9, R10)
 //   a4 bounds    a = ex^2+ey^2, b = 2(px ex + y_s ey), c = (px^2 + y_s^2) - r^2,
@@ -42,9 +43,18 @@ __device__ __forceinline__ bool ray_fp64(const GeomParams &gp, const double *__r
   double ck = views[3 * k], sk = views[3 * k + 1];
   tk = views[3 * k + 2];
 
-  double xd = dadd(-gp.cx, dmul(dadd((double)col, __ddiv_rn(dadd((double)u, 0.5), (double)gp.sub_x)), gp.dx));
+  // sub-pixel offset in its cell: centre (R8) or the N3 jitter of global ray R = i S + s
+  double ux = 0.5, uz = 0.5;
+  if (gp.jitter) {
+    const uint64_t R = (uint64_t)i * (uint64_t)(gp.sub_x * gp.sub_z) + (uint64_t)s;
+    const uint4 o = philox4x32_10(make_uint4(0xFFFFFFFFu, (uint32_t)R, (uint32_t)(R >> 32), gp.step),
+                                  make_uint2(gp.seed_lo, gp.seed_hi));
+    ux = (double)u01f(o.x);
+    uz = (double)u01f(o.y);
+  }
+  double xd = dadd(-gp.cx, dmul(dadd((double)col, __ddiv_rn(dadd((double)u, ux), (double)gp.sub_x)), gp.dx));
   double yd = gp.odd;
-  double zd = dadd(-gp.cz, dmul(dadd((double)row, __ddiv_rn(dadd((double)v, 0.5), (double)gp.sub_z)), gp.dz));
+  double zd = dadd(-gp.cz, dmul(dadd((double)row, __ddiv_rn(dadd((double)v, uz), (double)gp.sub_z)), gp.dz));
   double xs, ys = -gp.sod, zs;
   if (gp.beam == DINR_CONE) {
     xs = 0.0;
@@ -89,13 +99,17 @@ __device__ __forceinline__ bool ray_fp64(const GeomParams &gp, const double *__r
 
 __global__ void k_ray_setup(GeomParams gp, const double *__restrict__ views, const int64_t *__restrict__ idx,
                             int64_t n, double *__restrict__ rec64, float4 *__restrict__ rec32,
-                            int *__restrict__ flags) {
+                            uint2 *__restrict__ rid, int *__restrict__ flags) {
   const int S = gp.sub_x * gp.sub_z;
   int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (gid >= n * S) return;
   int64_t p = gid / S;
   int s = (int)(gid - p * S);
   double rr[9], tk;
+  if (rid) {  // global ray id, keys the N3 sample offsets in the MLP kernels
+    const uint64_t R = (uint64_t)idx[p] * (uint64_t)S + (uint64_t)s;
+    rid[gid] = make_uint2((uint32_t)R, (uint32_t)(R >> 32));
+  }
   if (!ray_fp64(gp, views, idx[p], s, rr, tk)) {
     atomicOr(flags, 1);
     if (rec64)

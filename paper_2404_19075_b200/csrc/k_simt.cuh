@@ -14,11 +14,12 @@ namespace dinr {
 __device__ __forceinline__ float sigmoid_acc(float z) { return 1.f / (1.f + expf(-z)); }
 
 __global__ void s_features(const float4 *__restrict__ rec32, int64_t nsamp, int n_s, const float *__restrict__ B,
-                           int C, float *__restrict__ h0) {
+                           int C, float *__restrict__ h0, Jitter jit) {
   int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= nsamp) return;
   int64_t ray = g / n_s;
-  float jj = (float)(g - ray * n_s) + 0.5f;
+  const uint32_t jr = (uint32_t)(g - ray * n_s);
+  float jj = (float)jr + sample_offset(jit, ray, jr);
   float4 a = rec32[2 * ray], b = rec32[2 * ray + 1];
   float rb[4] = {a.w, a.z + jj * b.z, a.y + jj * b.y, a.x + jj * b.x};  // (t, z, y, x), R12
   float *out = h0 + g * (2 * C);

@@ -28,6 +28,7 @@ struct DwParams {
   const float *B;
   int n_s, lg_ns;
   int64_t nsamp;
+  Jitter jit;
 };
 
 template <int H>
@@ -136,7 +137,7 @@ __global__ void __launch_bounds__(DwLayout<H>::NT, 1) k_tc_dw(DwParams p) {
     for (int64_t t = split; t < p.n_tiles; t += ks, ++it) {
       const int st = it % NST;
       const int64_t g = t * 128 + row;
-      const float4 rb = grff_coords(p.rec32, g, p.lg_ns, p.n_s, g < p.nsamp);
+      const float4 rb = grff_coords(p.rec32, g, p.lg_ns, p.n_s, g < p.nsamp, p.jit);
       if (it >= NST) mbar_wait(&empty[st], ((it / NST) - 1) & 1);
       const uint32_t sb = smem_u32(smem + st * LY::STAGE + LY::A_STAGE);
 #pragma unroll

@@ -21,6 +21,7 @@ namespace dinr {
 
 struct TcParams {
   const float4 *rec32;
+  Jitter jit;  // N3 sample placement
   int64_t nsamp;
   int n_s;
   int L;
@@ -139,7 +140,8 @@ __global__ void __launch_bounds__(128, 1) k_tc_mlp(TcParams p) {
       float rb0 = 0.f, rb1 = 0.f, rb2 = 0.f, rb3 = 0.f;
       if (valid) {
         int64_t ray = g / p.n_s;
-        float jj = (float)(g - ray * p.n_s) + 0.5f;
+        const uint32_t jr = (uint32_t)(g - ray * p.n_s);
+        float jj = (float)jr + sample_offset(p.jit, ray, jr);
         float4 ra = p.rec32[2 * ray], rbv = p.rec32[2 * ray + 1];
         rb0 = ra.w;                 // t
         rb1 = ra.z + jj * rbv.z;    // z

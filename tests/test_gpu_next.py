@@ -101,3 +101,113 @@ def test_phantom_mass_conservation_parallel(ctx, dev):
     D.phantom_project(ctx, prims, torch.arange(3 * N, device=dev), fh, combine="linear")
     tot = fh.double().view(3, N).sum(1).cpu().numpy()
     assert np.all(np.abs(tot - mass) <= 1e-6 * mass)
+
+
+# ---------------------------------------------------------------------------------------------
+# N3 randomized (stratified-jitter) sampling: the CUDA path against the oracle's Philox jitter.
+from test_gpu_parity import CASES, rel_linf, setup_case, tensor_errs  # noqa: E402
+
+JIT = dict(sampling="jitter", seed=0x1234ABCD5678, step=11)
+
+
+@pytest.mark.parametrize("beam", ["parallel", "fan", "cone"])
+def test_jitter_ray_records_bit_identical(ctx, dev, O, beam):
+    rng = np.random.default_rng(15)
+    g = dict(beam=beam, n_rows=37, n_cols=53, sub_x=2, sub_z=3 if beam == "cone" else 1, n_s=32, sod=31.0,
+             odd=17.5, pixel_dx=0.37, pixel_dz=0.41, offset_cx=9.7, offset_cz=7.3, fov_radius=10.1,
+             rot_center_x=0.61, z_lo=-8.0, z_hi=8.0, t_lo=0.0, t_hi=10.0)
+    M = 97
+    th = rng.uniform(-7, 7, M)
+    t = np.sort(rng.uniform(0, 10, M))
+    D.set_geometry(ctx, g, th, t)
+    D.set_sampling(ctx, "jitter", JIT["seed"], JIT["step"])
+    idx = rng.integers(0, M * g["n_rows"] * g["n_cols"], 4000)
+    S = g["sub_x"] * g["sub_z"]
+    rec = torch.zeros(len(idx) * S * 9, dtype=torch.float64, device=dev)
+    D.ray_records(ctx, torch.tensor(idx, device=dev), rec)
+    torch.cuda.synchronize()
+    ref, rc = O.rays(dict(g, **JIT), th, idx)
+    got = rec.cpu().numpy().reshape(len(idx), S, 9)
+    assert np.array_equal(got.view(np.uint64), ref.view(np.uint64))
+    mid, _ = O.rays(g, th, idx)
+    assert not np.array_equal(ref, mid)
+
+
+@pytest.mark.parametrize("precision,tol", [("bf16", 2e-3), ("fp32_verify", 1e-5)])
+@pytest.mark.parametrize("case", [0, 1, 2, 4])
+def test_jitter_projection_parity(ctx, dev, O, precision, tol, case):
+    name, over, fover, n = CASES[case]
+    g, th, t, f, B, prm = setup_case(ctx, dev, name, over, fover, precision, "beer")
+    D.set_sampling(ctx, "jitter", JIT["seed"], JIT["step"])
+    idx = synth.pixel_batch(name, n, seed=17, **over)
+    S = g["sub_x"] * g["sub_z"]
+    fhat = torch.zeros(n, device=dev)
+    psub = torch.zeros(n * S, device=dev)
+    D.project(ctx, torch.tensor(idx, device=dev), fhat, psub)
+    torch.cuda.synchronize()
+    rf, rp, rc = O.project(dict(g, **JIT), th, t, f, B, prm, idx)
+    assert rc == 0
+    assert rel_linf(psub.cpu().numpy().reshape(n, S), rp) <= tol
+    assert rel_linf(fhat.cpu().numpy(), rf) <= tol
+    # and the jitter is really on: the midpoint oracle differs
+    mf, _, _ = O.project(g, th, t, f, B, prm, idx)
+    assert rel_linf(mf, rf) > 1e-4
+
+
+@pytest.mark.parametrize("precision,tol", [("bf16", 1e-2), ("fp32_verify", 1e-4)])
+@pytest.mark.parametrize("case", [0, 1, 4])
+def test_jitter_gradient_parity(ctx, dev, O, precision, tol, case):
+    name, over, fover, n = CASES[case]
+    g, th, t, f, B, prm = setup_case(ctx, dev, name, over, fover, precision, "beer")
+    D.set_sampling(ctx, "jitter", JIT["seed"], JIT["step"])
+    gj = dict(g, **JIT)
+    idx = synth.pixel_batch(name, n, seed=18, **over)
+    y, _, _ = O.project_exact(gj, th, t, synth.phantom(name), idx, "beer")
+    y = y.astype(np.float32)
+    P = synth.param_count(f["C"], f["L"])
+    grad = torch.zeros(P + 1, device=dev)
+    D.project_and_grad(ctx, torch.tensor(idx, device=dev), torch.tensor(y, device=dev), grad)
+    torch.cuda.synchronize()
+    ref, rc = O.project_and_grad(gj, th, t, f, B, prm, idx, y)
+    got = grad.cpu().numpy()
+    assert max(tensor_errs(got[:P], ref[:P], f["C"], f["L"])) <= tol
+    assert abs(got[P] - ref[P]) <= max(tol, 1e-6) * abs(ref[P])
+
+
+def test_jitter_keyed_by_pixel_not_batch(ctx, dev):
+    """The draws depend on (seed, step, pixel index) only: a permuted batch gives the permuted
+    projections bit for bit, a new step changes them, the same step reproduces them."""
+    name = "fan512"
+    g, th, t, f, B, prm = setup_case(ctx, dev, name, {}, {}, "bf16", "beer")
+    idx = torch.tensor(synth.pixel_batch(name, 64, seed=19), device=dev)
+    perm = torch.randperm(64, device=dev)
+
+    def run(ix, step):
+        D.set_sampling(ctx, "jitter", 99, step)
+        out = torch.zeros(ix.numel(), device=dev)
+        D.project(ctx, ix, out)
+        return out
+
+    a = run(idx, 1)
+    assert torch.equal(run(idx[perm], 1), a[perm])
+    assert torch.equal(run(idx, 1), a)
+    assert not torch.equal(run(idx, 2), a)
+    D.set_sampling(ctx, "midpoint")
+
+
+def test_jitter_phantom_parity(ctx, dev, O):
+    g = dict(beam="cone", n_rows=8, n_cols=12, sub_x=2, sub_z=2, n_s=32, sod=40.0, odd=30.0, pixel_dx=1.5,
+             pixel_dz=1.5, offset_cx=9.0, offset_cz=6.0, fov_radius=12.0, rot_center_x=0.4, z_lo=-6, z_hi=6,
+             t_lo=0.0, t_hi=100.0)
+    rng = np.random.default_rng(23)
+    M = 10
+    theta, t = rng.uniform(0, 2 * np.pi, M), np.linspace(0, 100, M)
+    D.set_geometry(ctx, g, theta, t)
+    D.set_sampling(ctx, "jitter", 5, 3)
+    idx = rng.choice(M * 96, 400, replace=False)
+    fh = torch.zeros(len(idx), device=dev)
+    ps = torch.zeros(len(idx) * 4, device=dev)
+    D.phantom_project(ctx, PRIMS, torch.tensor(idx, device=dev), fh, ps, combine="beer")
+    rf, rp, rc = O.project_exact(dict(g, sampling="jitter", seed=5, step=3), theta, t, PRIMS, idx, "beer")
+    assert np.max(np.abs(fh.cpu().numpy() - rf)) <= 1e-6 * np.max(np.abs(rf))
+    assert np.max(np.abs(ps.cpu().numpy().reshape(-1, 4) - rp)) <= 1e-6 * np.max(np.abs(rp))
