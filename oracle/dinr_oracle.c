@@ -666,6 +666,53 @@ int or_project_exact(const or_geom *g, const double *theta, const double *t, int
   return err ? -1 : 0;
 }
 
+/* N4 ------------------------------------------------------------ */
+void or_default_grid(const or_geom *g, or_grid *out) {
+  /* "a spatial resolution equal to the detector pixel size divided by the geometric
+   * magnification ... one for parallel-beam and ... the ratio of the source-to-detector
+   * distance and the source-to-object distance for cone-beam" */
+  double mag = g->beam == 0 ? 1.0 : (g->sod + g->odd) / g->sod;
+  double vx = g->dx / mag, vz = g->dz / mag;
+  out->vx = vx;
+  out->vy = vx;
+  out->vz = vz;
+  out->nx = (int64_t)ceil(2.0 * g->r / vx);
+  out->ny = out->nx;
+  out->nz = (int64_t)ceil((g->z_hi - g->z_lo) / vz);
+  if (out->nz < 1) out->nz = 1;
+  out->x0 = g->xs0 - 0.5 * (double)out->nx * vx;
+  out->y0 = -0.5 * (double)out->ny * vx;
+  out->z0 = 0.5 * (g->z_lo + g->z_hi) - 0.5 * (double)out->nz * vz;
+}
+
+void or_voxelize(const or_geom *g, const or_field *f, const double *B, const double *params, const or_grid *grid,
+                 double t, int64_t k_begin, int64_t k_count, double *out) {
+  net_t nt = make_net(f, B, params);
+  int64_t plane = grid->nx * grid->ny, n = plane * k_count;
+#pragma omp parallel
+  {
+    double *hs = (double *)malloc(sizeof(double) * (size_t)(nt.L + 1) * nt.H);
+    double *zs = (double *)malloc(sizeof(double) * (size_t)nt.L * nt.H);
+#pragma omp for schedule(static)
+    for (int64_t v = 0; v < n; ++v) {
+      int64_t i = v % grid->nx, j = (v / grid->nx) % grid->ny, k = k_begin + v / plane;
+      double x = grid->x0 + ((double)i + 0.5) * grid->vx;
+      double y = grid->y0 + ((double)j + 0.5) * grid->vy;
+      double z = grid->z0 + ((double)k + 0.5) * grid->vz;
+      double px = x - g->xs0;
+      if (px * px + y * y <= g->r * g->r) { /* FOV cylinder, R25 */
+        double rb[4];
+        normalize(g, x, y, z, t, rb);
+        out[v] = mlp_forward(&nt, rb, hs, zs);
+      } else {
+        out[v] = 0.0;
+      }
+    }
+    free(hs);
+    free(zs);
+  }
+}
+
 void or_adam_step(double *param, const double *grad, double *m, double *v, int64_t n, double lr, double b1,
                   double b2, double eps, int64_t step) {
   double c1 = 1.0 - pow(b1, (double)step), c2 = 1.0 - pow(b2, (double)step);

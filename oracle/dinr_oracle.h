@@ -79,6 +79,22 @@ int or_fov_delta_bounds(const double src[2], const double dst[2], double xs0, do
 /* Ray records for n pixels: per sub-ray s (s = v*sub_x + u) 9 doubles
  * {o.x,o.y,o.z, d.x,d.y,d.z, delta_min, delta_max, chord}.  Out: rec[n*S*9].
  * Returns 0, or -1 if an index is out of range (its records are zeroed). */
+/* N4 voxel grid: voxel (i,j,k) centre (x0 + (i+1/2) vx, y0 + (j+1/2) vy, z0 + (k+1/2) vz). */
+typedef struct {
+  int64_t nx, ny, nz;
+  double x0, y0, z0;
+  double vx, vy, vz;
+} or_grid;
+
+/* voxel = pixel / magnification (1 parallel; (sod+odd)/sod fan, cone), grid
+ * covering [xs0 - r, xs0 + r] x [-r, r] x [z_lo, z_hi], centred (R25). */
+void or_default_grid(const or_geom *g, or_grid *out);
+
+/* mu at the voxel centres of planes [k_begin, k_begin + k_count) at time t:
+ * out[((k - k_begin) ny + j) nx + i] = M(normalize(centre, t)), 0 outside the FOV cylinder (R25). */
+void or_voxelize(const or_geom *g, const or_field *f, const double *B, const double *params, const or_grid *grid,
+                 double t, int64_t k_begin, int64_t k_count, double *out);
+
 /* Philox4x32-10 (Salmon et al. 2011), the counter-based generator of N3: out = bijection of ctr
  * under key.  u01(x) = (x >> 8) 2^-24, exactly representable in fp32 and fp64. */
 void or_philox4x32(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);

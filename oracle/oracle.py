@@ -50,6 +50,11 @@ class OrField(C.Structure):
                 ("mu0", C.c_double)]
 
 
+class OrGrid(C.Structure):
+    _fields_ = [("nx", C.c_int64), ("ny", C.c_int64), ("nz", C.c_int64), ("x0", C.c_double), ("y0", C.c_double),
+                ("z0", C.c_double), ("vx", C.c_double), ("vy", C.c_double), ("vz", C.c_double)]
+
+
 class OrPrim(C.Structure):
     _fields_ = [("kind", C.c_int32), ("pad", C.c_int32), ("value", C.c_double),
                 ("c0", C.c_double * 3), ("vel", C.c_double * 3), ("a0", C.c_double * 3),
@@ -80,6 +85,9 @@ def lib():
         _lib.or_adam_step.argtypes = [d, d, d, d, i64, C.c_double, C.c_double, C.c_double, C.c_double, i64]
         _lib.or_philox4x32.argtypes = [C.POINTER(C.c_uint32), C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]
         _lib.or_sample_offsets.argtypes = [C.POINTER(OrGeom), pi64, i64, d, d]
+        _lib.or_default_grid.argtypes = [C.POINTER(OrGeom), C.POINTER(OrGrid)]
+        _lib.or_voxelize.argtypes = [C.POINTER(OrGeom), C.POINTER(OrField), d, d, C.POINTER(OrGrid), C.c_double, i64, i64,
+                                     d]
         _lib.or_line_integral_exact.restype = C.c_double
         _lib.or_line_integral_exact.argtypes = [C.POINTER(OrPrim), i32, d, d, C.c_double, C.c_double, C.c_double]
     return _lib
@@ -154,6 +162,26 @@ def sample_offsets(g, idx):
     gs = geom_struct(g)
     lib().or_sample_offsets(C.byref(gs), idx.ctypes.data_as(C.POINTER(C.c_int64)), len(idx), _dp(u), _dp(uxz))
     return u, uxz
+
+
+_GRID_KEYS = ("nx", "ny", "nz", "x0", "y0", "z0", "vx", "vy", "vz")
+
+
+def default_grid(g):
+    """N4 default voxel grid (pixel / magnification over the FOV box) as a dict."""
+    out = OrGrid()
+    lib().or_default_grid(C.byref(geom_struct(g)), C.byref(out))
+    return {k: getattr(out, k) for k in _GRID_KEYS}
+
+
+def voxelize(g, f, B, params, grid, t, k_begin=0, k_count=None):
+    """N4: mu at the voxel centres of z planes [k_begin, k_begin + k_count) -> [k_count, ny, nx]."""
+    k_count = grid["nz"] - k_begin if k_count is None else k_count
+    out = np.zeros((k_count, grid["ny"], grid["nx"]))
+    gr = OrGrid(*[grid[k] for k in _GRID_KEYS])
+    lib().or_voxelize(C.byref(geom_struct(g)), C.byref(field_struct(f)), _dp(_f64(B)), _dp(_f64(params)),
+                      C.byref(gr), float(t), int(k_begin), int(k_count), _dp(out))
+    return out
 
 
 def rays(g, theta, idx):
