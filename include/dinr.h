@@ -131,6 +131,39 @@ dinr_status dinr_set_geometry(dinr_ctx *ctx, const dinr_geometry *g, const doubl
  * Error: DINR_EINVAL for an unknown mode. */
 dinr_status dinr_set_sampling(dinr_ctx *ctx, dinr_sampling mode, uint64_t seed, uint32_t step);
 
+/* ---------------------------------------------------------------------------------------------
+ * N4 inference voxelization: the trained field on a regular 3D grid at
+ * a view time.  Voxel (i, j, k), 0 <= i < nx etc., has centre
+ *   (x0 + (i + 1/2) vx, y0 + (j + 1/2) vy, z0 + (k + 1/2) vz)    (object frame, lengths as geometry). */
+typedef struct {
+  int64_t nx, ny, nz;
+  double x0, y0, z0;  /* lower corner of voxel (0, 0, 0) */
+  double vx, vy, vz;  /* voxel size */
+} dinr_voxel_grid;
+
+/* The paper's grid: voxel = detector pixel / geometric magnification (1 for
+ * parallel, (sod + odd) / sod for fan and cone: source-to-detector over source-to-object), i.e.
+ * vx = vy = pixel_dx / mag, vz = pixel_dz / mag, covering the FOV box [x_s0 - r, x_s0 + r] x
+ * [-r, r] x [z_lo, z_hi] with nx = ny = ceil(2r / vx), nz = ceil((z_hi - z_lo) / vz), centred on
+ * the box.  Host only; requires dinr_set_geometry (else DINR_ESTATE). */
+dinr_status dinr_default_grid(dinr_ctx *ctx, dinr_voxel_grid *out);
+
+/* mu(x, t) = mu0 (w_o . h_L + b_o) (R6) at the voxel centres of the z planes
+ * [k_begin, k_begin + k_count) at time t (normalized like the training samples):
+ *   out_dev[((k - k_begin) ny + j) nx + i]  fp32, device memory of nx ny k_count floats;
+ * 0 for centres outside the FOV cylinder (x - x_s0)^2 + y^2 <= r^2 (R25).  Precision as set by
+ * dinr_set_field_weights.  Stream-ordered.  DINR_EINVAL for an empty / out-of-range slab. */
+dinr_status dinr_voxelize(dinr_ctx *ctx, const dinr_voxel_grid *grid, double t, int64_t k_begin, int64_t k_count,
+                          float *out_dev, void *stream);
+
+/* Volumes at the view times t_m, m in [view_begin, view_begin + n_views) (the paper voxelizes at
+ * the acquisition times), streamed to a raw little-endian fp32 file laid out [m][k][j][i]:
+ * slabs of slab_planes z planes are computed on the GPU while the previous slab is copied to
+ * pinned host memory and written (double buffering).  Synchronous; DINR_EINVAL on a bad range,
+ * DINR_ECUDA on an I/O error (message names the file). */
+dinr_status dinr_voxelize_to_file(dinr_ctx *ctx, const dinr_voxel_grid *grid, int64_t view_begin, int64_t n_views,
+                                  const char *path, int64_t slab_planes);
+
 /* Field weights: B_dev = GRFF matrix (C x 4 fp32, columns t,z,y,x, frozen, R12);
  * params_dev = P fp32 trainable parameters (D5 layout).  Packs bf16 tensor-core operands on
  * `stream` (stream-ordered; the caller may overwrite params_dev after this on the same

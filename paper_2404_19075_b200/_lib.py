@@ -29,8 +29,17 @@ EXPORTS = [
     "dinr_project_and_grad_host", "dinr_ray_records", "dinr_nccl_unique_id", "dinr_comm_init",
     "dinr_allreduce_grads", "dinr_get_device_status", "dinr_set_timing", "dinr_read_timing",
     "dinr_launch_count", "dinr_adam_step", "dinr_phantom_project", "dinr_set_sampling",
+    "dinr_default_grid", "dinr_voxelize", "dinr_voxelize_to_file",
 ]
 SAMPLINGS = {"midpoint": 0, "jitter": 1}
+
+
+class VoxelGrid(C.Structure):
+    _fields_ = [("nx", C.c_int64), ("ny", C.c_int64), ("nz", C.c_int64), ("x0", C.c_double), ("y0", C.c_double),
+                ("z0", C.c_double), ("vx", C.c_double), ("vy", C.c_double), ("vz", C.c_double)]
+
+
+GRID_KEYS = ("nx", "ny", "nz", "x0", "y0", "z0", "vx", "vy", "vz")
 
 
 class DinrError(RuntimeError):
@@ -94,6 +103,9 @@ def load(path: str = SO_PATH):
         "dinr_status_string": (C.c_char_p, [st]),
         "dinr_set_geometry": (st, [vp, C.POINTER(Geometry), d, d, i64]),
         "dinr_set_sampling": (st, [vp, C.c_int, C.c_uint64, C.c_uint32]),
+        "dinr_default_grid": (st, [vp, C.POINTER(VoxelGrid)]),
+        "dinr_voxelize": (st, [vp, C.POINTER(VoxelGrid), C.c_double, i64, i64, vp, vp]),
+        "dinr_voxelize_to_file": (st, [vp, C.POINTER(VoxelGrid), i64, i64, C.c_char_p, i64]),
         "dinr_set_field_weights": (st, [vp, C.POINTER(FieldDesc), vp, vp, vp]),
         "dinr_project": (st, [vp, vp, i64, vp, vp, vp, vp, vp]),
         "dinr_project_and_grad": (st, [vp, vp, i64, vp, vp, C.c_int, vp]),
@@ -171,6 +183,28 @@ def set_sampling(ctx, mode: str = "midpoint", seed: int = 0, step: int = 0):
     """N3 sample placement for the following calls: "midpoint" (R8) or "jitter" (Philox)."""
     _check(ctx, load().dinr_set_sampling(ctx, SAMPLINGS[mode], int(seed) & 0xFFFFFFFFFFFFFFFF,
                                          int(step) & 0xFFFFFFFF))
+
+
+def default_grid(ctx) -> dict:
+    """N4: the paper's voxel grid (detector pixel / magnification over the FOV box)."""
+    gr = VoxelGrid()
+    _check(ctx, load().dinr_default_grid(ctx, C.byref(gr)))
+    return {k: getattr(gr, k) for k in GRID_KEYS}
+
+
+def voxelize(ctx, grid: dict, t: float, out, k_begin: int = 0, k_count: int | None = None, stream=None):
+    """N4: mu at the voxel centres of z planes [k_begin, k_begin + k_count) into out (device fp32)."""
+    k_count = grid["nz"] - k_begin if k_count is None else k_count
+    gr = VoxelGrid(*[grid[k] for k in GRID_KEYS])
+    _check(ctx, load().dinr_voxelize(ctx, C.byref(gr), float(t), int(k_begin), int(k_count), _ptr(out),
+                                     _stream(stream, out)))
+
+
+def voxelize_to_file(ctx, grid: dict, path: str, view_begin: int = 0, n_views: int = 1, slab_planes: int = 64):
+    """N4: volumes at the view times streamed to a raw fp32 file [view][z][y][x]."""
+    gr = VoxelGrid(*[grid[k] for k in GRID_KEYS])
+    _check(ctx, load().dinr_voxelize_to_file(ctx, C.byref(gr), int(view_begin), int(n_views), path.encode(),
+                                             int(slab_planes)))
 
 
 def set_field_weights(ctx, f: dict, B, params, precision: str = "bf16", stream=None):

@@ -22,6 +22,7 @@
 #include "k_tc_mlp.cuh"
 #include "k_fused.cuh"
 #include "k_fused2.cuh"
+#include "k_infer.cuh"
 #include "k_phantom.cuh"
 #include "nccl_dl.cuh"
 
@@ -770,6 +771,7 @@ dinr_status dinr_set_geometry(dinr_ctx *c, const dinr_geometry *g, const double 
   c->geom = *g;
   c->M = M;
   c->S = g->sub_x * g->sub_z;
+  c->h_t.assign(t, t + M);
   c->have_geom = true;
   return DINR_OK;
 }
@@ -1029,5 +1031,250 @@ dinr_status dinr_read_timing(dinr_ctx *c, int which, double *ms, int64_t *launch
 }
 
 int64_t dinr_launch_count(const dinr_ctx *c) { return c ? c->launches : 0; }
+
+}  // extern "C"
+
+// ------------------------------------------------------------------------------------------------
+// N4 inference voxelization
+namespace {
+
+VoxGrid vox_grid(const dinr_ctx *c, const dinr_voxel_grid &g, double t, int64_t k0) {
+  const dinr_geometry &ge = c->geom;
+  VoxGrid v;
+  v.nx = g.nx;
+  v.ny = g.ny;
+  v.k0 = k0;
+  v.x0 = g.x0;
+  v.y0 = g.y0;
+  v.z0 = g.z0;
+  v.vx = g.vx;
+  v.vy = g.vy;
+  v.vz = g.vz;
+  v.xs0 = ge.rot_center_x;
+  v.r = ge.fov_radius;
+  v.zc = 0.5 * (ge.z_lo + ge.z_hi);
+  v.zh = 0.5 * (ge.z_hi - ge.z_lo);
+  const double tc = 0.5 * (ge.t_lo + ge.t_hi), th = 0.5 * (ge.t_hi - ge.t_lo);
+  v.tbar = th > 0.0 ? (float)((t - tc) / th) : 0.f;
+  return v;
+}
+
+template <int H>
+bool infer_fits(const dinr_ctx *c) {
+  return InferLayout<H>::smem_bytes(c->L) <= 227 * 1024;
+}
+
+template <int H>
+dinr_status launch_infer(dinr_ctx *c, const VoxGrid &vg, int64_t n_vox, float *out, cudaStream_t st) {
+  if (c->field.precision == DINR_BF16 && H <= 128 && infer_fits<H>(c)) {
+    InferParams p{};
+    p.vg = vg;
+    p.n_vox = n_vox;
+    p.L = c->L;
+    p.mu0 = (float)c->field.mu0;
+    p.params = c->d_params;
+    p.B = c->d_B;
+    p.wpack_half = c->d_wpack_half;
+    p.out = out;
+    const size_t smem = InferLayout<H>::smem_bytes(c->L);
+    dinr_status s = set_smem(c, k_infer<H>, smem);
+    if (s) return s;
+    const int64_t groups = (n_vox + 255) / 256;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(groups, c->sm_count));
+    Launch L_(c, T_FWD, st);
+    k_infer<H><<<grid, InferLayout<H>::NT, smem, st>>>(p);
+    CUDA_TRY(c, cudaGetLastError());
+    return DINR_OK;
+  }
+  // general path (H = 256 or layers that do not fit): K2 in grid mode, weights streamed
+  TcParams p{};
+  p.nsamp = n_vox;
+  p.n_s = 1;
+  p.L = c->L;
+  p.resident = tc_resident(H, c->L) ? 1 : 0;
+  p.mu0 = (float)c->field.mu0;
+  p.params = c->d_params;
+  p.B = c->d_B;
+  p.wpack = c->d_wpack;
+  p.grid_mode = 1;
+  p.vg = vg;
+  p.vout = out;
+  const size_t smem = TcLayout<H>::smem_bytes(c->L, p.resident != 0);
+  dinr_status s = set_smem(c, k_tc_mlp<H, false>, smem);
+  if (s) return s;
+  const int64_t tiles = (n_vox + 127) / 128;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)c->sm_count * tc_occupancy(c)));
+  Launch L_(c, T_FWD, st);
+  k_tc_mlp<H, false><<<grid, 128, smem, st>>>(p);
+  CUDA_TRY(c, cudaGetLastError());
+  return DINR_OK;
+}
+
+dinr_status simt_voxelize(dinr_ctx *c, const VoxGrid &vg, int64_t n_vox, float *out, cudaStream_t st) {
+  const int H = c->H, L = c->L;
+  const int64_t per_pix = (int64_t)c->S * c->geom.samples_per_ray;
+  Plan pl;
+  dinr_status s = ensure_plan(c, (n_vox + per_pix - 1) / per_pix, false, false, pl);
+  if (s) return s;
+  {
+    Launch L_(c, T_FWD, st);
+    s_vox_features<<<(unsigned)((n_vox + 255) / 256), 256, 0, st>>>(vg, n_vox, c->d_B, c->C, pl.sh);
+  }
+  CUDA_TRY(c, cudaGetLastError());
+  const int64_t per = (int64_t)H * H + H;
+  for (int l = 0; l < L; ++l) {
+    SgemmArgs a{};
+    a.A = pl.sh + (size_t)l * n_vox * H;
+    a.sam = H;
+    a.sak = 1;
+    a.B = c->d_params + l * per;
+    a.sbk = 1;
+    a.sbn = H;
+    a.M = n_vox;
+    a.N = H;
+    a.K = H;
+    a.kchunk = H;
+    a.mode = 1;
+    a.ldc = H;
+    a.bias = c->d_params + l * per + (int64_t)H * H;
+    a.Z = pl.sz + (size_t)l * n_vox * H;
+    a.Hout = pl.sh + (size_t)(l + 1) * n_vox * H;
+    s = simt_gemm(c, a, 1, st, T_FWD);
+    if (s) return s;
+  }
+  {
+    Launch L_(c, T_FWD, st);
+    s_vox_head<<<(unsigned)((n_vox + 255) / 256), 256, 0, st>>>(vg, pl.sh + (size_t)L * n_vox * H, n_vox, H,
+                                                              c->d_params + L * per, (float)c->field.mu0, out);
+  }
+  CUDA_TRY(c, cudaGetLastError());
+  return DINR_OK;
+}
+
+dinr_status voxelize_slab(dinr_ctx *c, const dinr_voxel_grid &g, double t, int64_t k0, int64_t kn, float *out,
+                          cudaStream_t st) {
+  const VoxGrid vg = vox_grid(c, g, t, k0);
+  const int64_t n_vox = g.nx * g.ny * kn;
+  if (c->field.precision == DINR_FP32_VERIFY) return simt_voxelize(c, vg, n_vox, out, st);
+  switch (c->H) {
+    case 64: return launch_infer<64>(c, vg, n_vox, out, st);
+    case 128: return launch_infer<128>(c, vg, n_vox, out, st);
+    default: return launch_infer<256>(c, vg, n_vox, out, st);
+  }
+}
+
+bool grid_ok(const dinr_voxel_grid *g) {
+  return g && g->nx > 0 && g->ny > 0 && g->nz > 0 && g->vx > 0 && g->vy > 0 && g->vz > 0 &&
+         std::isfinite(g->x0) && std::isfinite(g->y0) && std::isfinite(g->z0) && g->nx * g->ny <= (int64_t)1 << 40;
+}
+
+}  // namespace
+
+extern "C" {
+
+dinr_status dinr_default_grid(dinr_ctx *c, dinr_voxel_grid *out) {
+  if (!c || !out) return DINR_EINVAL;
+  if (!c->have_geom) return fail(c, DINR_ESTATE, "geometry must be set first");
+  const dinr_geometry &g = c->geom;
+  const double mag = g.beam == DINR_PARALLEL ? 1.0 : (g.sod + g.odd) / g.sod;
+  const double vx = g.pixel_dx / mag, vz = g.pixel_dz / mag, r = g.fov_radius;
+  out->vx = out->vy = vx;
+  out->vz = vz;
+  out->nx = out->ny = (int64_t)std::ceil(2.0 * r / vx);
+  out->nz = std::max<int64_t>(1, (int64_t)std::ceil((g.z_hi - g.z_lo) / vz));
+  out->x0 = g.rot_center_x - 0.5 * (double)out->nx * vx;
+  out->y0 = -0.5 * (double)out->ny * vx;
+  out->z0 = 0.5 * (g.z_lo + g.z_hi) - 0.5 * (double)out->nz * vz;
+  return DINR_OK;
+}
+
+dinr_status dinr_voxelize(dinr_ctx *c, const dinr_voxel_grid *g, double t, int64_t k_begin, int64_t k_count,
+                          float *out_dev, void *stream) {
+  if (!c) return DINR_EINVAL;
+  if (!c->have_geom || !c->have_field) return fail(c, DINR_ESTATE, "geometry and field weights must be set first");
+  if (!grid_ok(g) || !out_dev || k_begin < 0 || k_count <= 0 || k_begin + k_count > g->nz || !std::isfinite(t))
+    return fail(c, DINR_EINVAL, "bad voxel grid or slab");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  return voxelize_slab(c, *g, t, k_begin, k_count, out_dev, (cudaStream_t)stream);
+}
+
+dinr_status dinr_voxelize_to_file(dinr_ctx *c, const dinr_voxel_grid *g, int64_t view_begin, int64_t n_views,
+                                  const char *path, int64_t slab_planes) {
+  if (!c) return DINR_EINVAL;
+  if (!c->have_geom || !c->have_field) return fail(c, DINR_ESTATE, "geometry and field weights must be set first");
+  if (!grid_ok(g) || !path || view_begin < 0 || n_views < 0 || view_begin + n_views > c->M || slab_planes <= 0)
+    return fail(c, DINR_EINVAL, "bad voxel grid, view range or slab size");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  FILE *fh = std::fopen(path, "wb");
+  if (!fh) return fail(c, DINR_ECUDA, std::string("cannot open ") + path);
+  const int64_t kp = std::min(slab_planes, g->nz);
+  const size_t slab = (size_t)(g->nx * g->ny * kp);
+  float *dbuf[2] = {nullptr, nullptr}, *hbuf[2] = {nullptr, nullptr};
+  cudaStream_t st = nullptr;
+  cudaEvent_t done[2] = {nullptr, nullptr};
+  dinr_status rs = DINR_OK;
+  auto cleanup = [&]() {
+    if (st) cudaStreamSynchronize(st);
+    for (int b = 0; b < 2; ++b) {
+      cudaFree(dbuf[b]);
+      cudaFreeHost(hbuf[b]);
+      if (done[b]) cudaEventDestroy(done[b]);
+    }
+    if (st) cudaStreamDestroy(st);
+    std::fclose(fh);
+  };
+  if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) {
+    cleanup();
+    return fail(c, DINR_ECUDA, "stream creation failed");
+  }
+  for (int b = 0; b < 2; ++b)
+    if (cudaMalloc(&dbuf[b], slab * sizeof(float)) != cudaSuccess ||
+        cudaMallocHost(&hbuf[b], slab * sizeof(float)) != cudaSuccess ||
+        cudaEventCreateWithFlags(&done[b], cudaEventDisableTiming) != cudaSuccess) {
+      cleanup();
+      return fail(c, DINR_ENOMEM, "voxel slab buffers");
+    }
+  // slab q: compute into dbuf[q%2], copy to hbuf[q%2], record done[q%2]; the host writes slab q-1
+  // while slab q is on the GPU
+  int64_t pending = -1, pending_n = 0;
+  int64_t q = 0;
+  for (int64_t m = view_begin; m < view_begin + n_views && rs == DINR_OK; ++m)
+    for (int64_t k0 = 0; k0 < g->nz && rs == DINR_OK; k0 += kp, ++q) {
+      const int64_t kn = std::min(kp, g->nz - k0);
+      const int b = (int)(q & 1);
+      if (pending >= 0 && (pending & 1) == b) {  // both buffers busy: drain the older one first
+        cudaEventSynchronize(done[b]);
+        if (std::fwrite(hbuf[b], sizeof(float), (size_t)pending_n, fh) != (size_t)pending_n)
+          rs = fail(c, DINR_ECUDA, std::string("write failed: ") + path);
+        pending = -1;
+      }
+      if (rs) break;
+      rs = voxelize_slab(c, *g, c->h_t[m], k0, kn, dbuf[b], st);
+      if (rs) break;
+      const int64_t n = g->nx * g->ny * kn;
+      if (cudaMemcpyAsync(hbuf[b], dbuf[b], (size_t)n * sizeof(float), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+          cudaEventRecord(done[b], st) != cudaSuccess) {
+        rs = fail(c, DINR_ECUDA, "slab copy failed");
+        break;
+      }
+      if (pending >= 0) {  // write the previous slab while this one computes
+        const int pb = (int)(pending & 1);
+        cudaEventSynchronize(done[pb]);
+        if (std::fwrite(hbuf[pb], sizeof(float), (size_t)pending_n, fh) != (size_t)pending_n)
+          rs = fail(c, DINR_ECUDA, std::string("write failed: ") + path);
+      }
+      pending = q;
+      pending_n = n;
+    }
+  if (rs == DINR_OK && pending >= 0) {
+    const int pb = (int)(pending & 1);
+    if (cudaEventSynchronize(done[pb]) != cudaSuccess)
+      rs = fail(c, DINR_ECUDA, "slab compute failed");
+    else if (std::fwrite(hbuf[pb], sizeof(float), (size_t)pending_n, fh) != (size_t)pending_n)
+      rs = fail(c, DINR_ECUDA, std::string("write failed: ") + path);
+  }
+  cleanup();
+  return rs;
+}
 
 }  // extern "C"

@@ -64,6 +64,7 @@ struct dinr_ctx {
   int64_t M = 0;
   int S = 1;
   double *d_views = nullptr;  // M x 3 {cos theta, sin theta, t}
+  std::vector<double> h_t;    // view times (host copy, N4)
   // N3 sample placement (dinr_set_sampling)
   int sampling = DINR_MIDPOINT;
   uint64_t seed = 0;

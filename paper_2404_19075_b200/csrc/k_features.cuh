@@ -4,6 +4,7 @@
 // evaluated at the ray-sample coordinates from the fp32 ray records (R6, R9).
 #pragma once
 #include "internal.cuh"
+#include "k_geometry.cuh"
 #include "ptx_sm100.cuh"
 
 namespace dinr {
@@ -41,6 +42,32 @@ __device__ __forceinline__ void grff8(const float4 *sB4, int c0, float4 rb, uint
     pc[q] = pack_bf16x2(cs[0], cs[1]);
     ps[q] = pack_bf16x2(sn[0], sn[1]);
   }
+}
+
+// N4 voxel grid slab: voxel v of the launch -> (i, j, k) = (v % nx, (v / nx) % ny, k0 + v / (nx ny)),
+// centre (x0 + (i + 1/2) vx, y0 + (j + 1/2) vy, z0 + (k + 1/2) vz) at normalized time tbar.
+struct VoxGrid {
+  int64_t nx, ny, k0;
+  double x0, y0, z0, vx, vy, vz;
+  double xs0, r, zc, zh;  // normalization (R11) and FOV cylinder
+  float tbar;
+};
+
+// Normalized (t, z, y, x) of voxel v (fp64 centre, rounded once to fp32) and whether the centre
+// lies in the FOV cylinder (x - x_s0)^2 + y^2 <= r^2, decided in fp64 without contraction.
+__device__ __forceinline__ float4 voxel_coords(const VoxGrid &vg, int64_t v, bool &inside) {
+  const int64_t i = v % vg.nx, j = (v / vg.nx) % vg.ny, k = vg.k0 + v / (vg.nx * vg.ny);
+  const double x = dadd(vg.x0, dmul(dadd((double)i, 0.5), vg.vx));
+  const double y = dadd(vg.y0, dmul(dadd((double)j, 0.5), vg.vy));
+  const double z = dadd(vg.z0, dmul(dadd((double)k, 0.5), vg.vz));
+  const double px = dsub(x, vg.xs0);
+  inside = dadd(dmul(px, px), dmul(y, y)) <= dmul(vg.r, vg.r);
+  float4 r;
+  r.x = vg.tbar;
+  r.y = vg.zh > 0.0 ? (float)__ddiv_rn(dsub(z, vg.zc), vg.zh) : 0.f;
+  r.z = (float)__ddiv_rn(y, vg.r);
+  r.w = (float)__ddiv_rn(px, vg.r);
+  return r;
 }
 
 }  // namespace dinr

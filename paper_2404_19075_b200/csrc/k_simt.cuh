@@ -8,6 +8,7 @@
 //   backward  delta_l = e_l * swish'(z_l), dW_l = delta_l^T h_{l-1}, e_{l-1} = W_l^T delta_l
 #pragma once
 #include "internal.cuh"
+#include "k_features.cuh"
 
 namespace dinr {
 
@@ -23,6 +24,23 @@ __global__ void s_features(const float4 *__restrict__ rec32, int64_t nsamp, int 
   float4 a = rec32[2 * ray], b = rec32[2 * ray + 1];
   float rb[4] = {a.w, a.z + jj * b.z, a.y + jj * b.y, a.x + jj * b.x};  // (t, z, y, x), R12
   float *out = h0 + g * (2 * C);
+  for (int c = 0; c < C; ++c) {
+    float phi = B[4 * c] * rb[0] + B[4 * c + 1] * rb[1] + B[4 * c + 2] * rb[2] + B[4 * c + 3] * rb[3];
+    float sn, cs;
+    sincospif(2.f * phi, &sn, &cs);
+    out[c] = cs;
+    out[C + c] = sn;
+  }
+}
+
+// N4 voxels: GRFF features at the voxel centres (accurate sincospif, like s_features).
+__global__ void s_vox_features(VoxGrid vg, int64_t n_vox, const float *__restrict__ B, int C, float *__restrict__ h0) {
+  int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= n_vox) return;
+  bool inside;
+  const float4 r = voxel_coords(vg, v, inside);
+  const float rb[4] = {r.x, r.y, r.z, r.w};
+  float *out = h0 + v * (2 * C);
   for (int c = 0; c < C; ++c) {
     float phi = B[4 * c] * rb[0] + B[4 * c + 1] * rb[1] + B[4 * c + 2] * rb[2] + B[4 * c + 3] * rb[3];
     float sn, cs;
@@ -109,6 +127,19 @@ __global__ void s_head(const float *__restrict__ hL, int64_t nsamp, int H, const
   }
   for (int o = 16; o > 0; o >>= 1) mu += __shfl_xor_sync(0xffffffffu, mu, o);
   if ((threadIdx.x & 31) == 0 && g < nsamp) pchunk[g >> 5] = mu;
+}
+
+// N4 voxels: mu = mu0 (w_o . h_L + b_o) per voxel, 0 outside the FOV cylinder (R25).
+__global__ void s_vox_head(VoxGrid vg, const float *__restrict__ hL, int64_t n_vox, int H, const float *__restrict__ wo,
+                           float mu0, float *__restrict__ out) {
+  int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= n_vox) return;
+  bool inside;
+  (void)voxel_coords(vg, v, inside);
+  const float *h = hL + v * H;
+  float acc = 0.f;
+  for (int k = 0; k < H; ++k) acc += wo[k] * h[k];
+  out[v] = inside ? mu0 * (acc + wo[H]) : 0.f;
 }
 
 // delta = e * swish'(z), swish'(z) = sigma (1 + z (1 - sigma)); for the head layer

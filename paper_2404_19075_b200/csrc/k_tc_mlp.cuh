@@ -15,6 +15,7 @@
 // dL/db_o = sum u) with a warp transpose-reduction into registers.
 #pragma once
 #include "internal.cuh"
+#include "k_features.cuh"
 #include "ptx_sm100.cuh"
 
 namespace dinr {
@@ -36,6 +37,10 @@ struct TcParams {
   uint8_t *hstash, *dstash, *zstash;
   float *head_part;  // [gridDim.x][H+1]
   int64_t n_tiles;
+  // N4 inference: samples are voxel centres of vg, outputs per voxel to vout (forward only)
+  int grid_mode;
+  VoxGrid vg;
+  float *vout;
 };
 
 template <int H>
@@ -130,6 +135,7 @@ __global__ void __launch_bounds__(128, 1) k_tc_mlp(TcParams p) {
     const int row = tid;
     const int64_t g = (int64_t)tile * 128 + row;
     const bool valid = g < p.nsamp;
+    bool inside = false;
     float u_row = 0.f;
     if (TRAIN) {  // the previous tile's last bulk store must be done reading sA
       if (tid == 0) bulk_wait_read_all();
@@ -138,7 +144,13 @@ __global__ void __launch_bounds__(128, 1) k_tc_mlp(TcParams p) {
     // ---------------------------------------------------------------- a5/a6 features
     {
       float rb0 = 0.f, rb1 = 0.f, rb2 = 0.f, rb3 = 0.f;
-      if (valid) {
+      if (!TRAIN && p.grid_mode) {
+        const float4 r = voxel_coords(p.vg, valid ? g : 0, inside);
+        rb0 = r.x;
+        rb1 = r.y;
+        rb2 = r.z;
+        rb3 = r.w;
+      } else if (valid) {
         int64_t ray = g / p.n_s;
         const uint32_t jr = (uint32_t)(g - ray * p.n_s);
         float jj = (float)jr + sample_offset(p.jit, ray, jr);
@@ -284,9 +296,13 @@ __global__ void __launch_bounds__(128, 1) k_tc_mlp(TcParams p) {
     if (!TRAIN) {
       // a9 ray-chunk sum of M = mu0 (w_o . h_L + b_o) over the warp's 32 samples
       float mu = p.mu0 * (mu_acc + sWo[H]);
+      if (p.grid_mode) {
+        if (valid) p.vout[g] = inside ? mu : 0.f;
+      } else {
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) mu += __shfl_xor_sync(0xffffffffu, mu, o);
-      if (lane == 0 && valid) p.pchunk[g >> 5] = mu;
+        for (int o = 16; o > 0; o >>= 1) mu += __shfl_xor_sync(0xffffffffu, mu, o);
+        if (lane == 0 && valid) p.pchunk[g >> 5] = mu;
+      }
     } else {
       float us = u_row;
 #pragma unroll
