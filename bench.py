@@ -54,6 +54,26 @@ def peaks():
         return 1590.0, 1400.0, 6650.0, "fallback"
 
 
+def profiled_traffic(workload, kernel_class, path_kind):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu --set full capture
+    (profiles/traffic.json, written by tools/ncu_summary.py traffic), or None if that capture is
+    not for this workload / kernel."""
+    names = {"backward": {0: "k_tc_mlp", 1: "k_fused<", 2: "k_fused2<"}.get(path_kind, ""), "dw": "k_tc_dw",
+             "forward": "k_tc_mlp", "rays": "k_ray_setup", "loss": "k_loss"}
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            tr = json.load(fh)
+    except Exception:
+        return None
+    if tr.get("workload") != workload:
+        return None
+    want = names.get(kernel_class, "?")
+    for k, v in tr.get("kernels", {}).items():
+        if want and want in k:
+            return v
+    return None
+
+
 # ---------------------------------------------------------------------------- clocks
 class ClockSampler:
     """Polls nvidia-smi (one query every ~200 ms) in a background thread."""
@@ -234,6 +254,7 @@ def main():
     stream = torch.cuda.current_stream(dev)
     D.set_field_weights(ctx, f, B, params, stream=stream)
     pdist.init_comm(ctx, rank, world)
+    path_kind, path_nf = D.train_path(ctx, n)
 
     # inputs resident in HBM: a pool of distinct per-step batches from this rank's view shard
     pool = 4
@@ -337,8 +358,8 @@ def main():
         fps = flops_per_sample(L, H)
         # per-kernel algorithmic work per launch
         nsamp = n * S * ns
-        fused = ktimes["forward"][1] == 0  # k_fused: forward + loss + dX + top-nf dW in one kernel
-        nf = min(L, 512 // H - 1) if fused else 0
+        fused = path_kind > 0  # k_fused/k_fused2: forward + loss + dX + top-nf dW in one kernel
+        nf = path_nf
         alg = {
             "forward": ("tensor", 2.0 * L * H * H * nsamp),
             "backward": ("tensor", 2.0 * ((L + (L - 1) + nf) if fused else (L - 1)) * H * H * nsamp),
@@ -354,12 +375,12 @@ def main():
         if bound == "tensor":
             achieved = work / avg_s / 1e12
             roof = {"bound": "tensor", "achieved": achieved, "peak": tf_burst, "unit": "TFLOP/s",
-                    "frac": achieved / tf_burst, "traffic": None, "kernel": dom,
+                    "frac": achieved / tf_burst, "traffic": profiled_traffic(name, dom, path_kind), "kernel": dom,
                     "peak_source": f"{peak_src} bf16 dense (burst)"}
         else:
             achieved = work / avg_s / 1e9
             roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                    "traffic": None, "kernel": dom, "peak_source": f"{peak_src} HBM copy"}
+                    "traffic": profiled_traffic(name, dom, path_kind), "kernel": dom, "peak_source": f"{peak_src} HBM copy"}
         step_tflops = value * fps / 1e12
         base_rate, base_px, base_dt = (None, 0, 0.0)
         if args.cpu_baseline_seconds > 0 and world == 1:

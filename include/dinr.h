@@ -258,6 +258,13 @@ dinr_status dinr_set_timing(dinr_ctx *ctx, int enable);
 dinr_status dinr_read_timing(dinr_ctx *ctx, int which, double *ms, int64_t *launches, int reset);
 int64_t dinr_launch_count(const dinr_ctx *ctx);
 
+/* Which training path dinr_project_and_grad takes for a batch of n pixels with the current
+ * geometry and weights (host query, no device work): *fused_kernel = 0 split path (K2/K3/K5),
+ * 1 one-stream fused kernel, 2 two-stream fused kernel; *fused_dw_layers = number of top layers
+ * whose dW accumulate inside the fused kernel (the rest go through the dW GEMM).  For the
+ * roofline bookkeeping of bench.py.  DINR_ESTATE before weights are set. */
+dinr_status dinr_train_path(dinr_ctx *ctx, int64_t n, int32_t *fused_kernel, int32_t *fused_dw_layers);
+
 #ifdef __cplusplus
 }
 #endif

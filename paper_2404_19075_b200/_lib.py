@@ -29,7 +29,7 @@ EXPORTS = [
     "dinr_project_and_grad_host", "dinr_ray_records", "dinr_nccl_unique_id", "dinr_comm_init",
     "dinr_allreduce_grads", "dinr_get_device_status", "dinr_set_timing", "dinr_read_timing",
     "dinr_launch_count", "dinr_adam_step", "dinr_phantom_project", "dinr_set_sampling",
-    "dinr_default_grid", "dinr_voxelize", "dinr_voxelize_to_file",
+    "dinr_default_grid", "dinr_voxelize", "dinr_voxelize_to_file", "dinr_train_path",
 ]
 SAMPLINGS = {"midpoint": 0, "jitter": 1}
 
@@ -104,6 +104,7 @@ def load(path: str = SO_PATH):
         "dinr_set_geometry": (st, [vp, C.POINTER(Geometry), d, d, i64]),
         "dinr_set_sampling": (st, [vp, C.c_int, C.c_uint64, C.c_uint32]),
         "dinr_default_grid": (st, [vp, C.POINTER(VoxelGrid)]),
+        "dinr_train_path": (st, [vp, i64, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
         "dinr_voxelize": (st, [vp, C.POINTER(VoxelGrid), C.c_double, i64, i64, vp, vp]),
         "dinr_voxelize_to_file": (st, [vp, C.POINTER(VoxelGrid), i64, i64, C.c_char_p, i64]),
         "dinr_set_field_weights": (st, [vp, C.POINTER(FieldDesc), vp, vp, vp]),
@@ -183,6 +184,13 @@ def set_sampling(ctx, mode: str = "midpoint", seed: int = 0, step: int = 0):
     """N3 sample placement for the following calls: "midpoint" (R8) or "jitter" (Philox)."""
     _check(ctx, load().dinr_set_sampling(ctx, SAMPLINGS[mode], int(seed) & 0xFFFFFFFFFFFFFFFF,
                                          int(step) & 0xFFFFFFFF))
+
+
+def train_path(ctx, n: int):
+    """(fused kernel: 0 split / 1 one-stream / 2 two-stream, number of TMEM-fused dW layers)."""
+    fk, nf = C.c_int32(), C.c_int32()
+    _check(ctx, load().dinr_train_path(ctx, int(n), C.byref(fk), C.byref(nf)))
+    return fk.value, nf.value
 
 
 def default_grid(ctx) -> dict:

@@ -1032,6 +1032,16 @@ dinr_status dinr_read_timing(dinr_ctx *c, int which, double *ms, int64_t *launch
 
 int64_t dinr_launch_count(const dinr_ctx *c) { return c ? c->launches : 0; }
 
+dinr_status dinr_train_path(dinr_ctx *c, int64_t n, int32_t *fused_kernel, int32_t *fused_dw_layers) {
+  if (!c || !fused_kernel || !fused_dw_layers || n < 0) return DINR_EINVAL;
+  if (!c->have_geom || !c->have_field) return fail(c, DINR_ESTATE, "geometry and field weights must be set first");
+  Plan pl;
+  plan_layout(c, std::max<int64_t>(n, 1), true, false, pl, nullptr);
+  *fused_kernel = pl.fused ? (pl.fused2 ? 2 : 1) : 0;
+  *fused_dw_layers = pl.fused ? pl.nf : 0;
+  return DINR_OK;
+}
+
 }  // extern "C"
 
 // ------------------------------------------------------------------------------------------------
