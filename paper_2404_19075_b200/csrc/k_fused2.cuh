@@ -45,10 +45,11 @@ constexpr int kF2TileArrivals = 256;
 constexpr int kF2TileArrivals = 8;
 #endif
 
+
 template <int H>
 struct Fused2Layout {
   static constexpr int EPI = 512;                 // 2 warpgroups x 8 warps
-  static constexpr int NT = EPI + 32;             // + control warp
+  static constexpr int NT = EPI + 64;             // + MMA warp + copy warp
   static constexpr uint32_t TILE = H * 256u;      // one 128-row bf16 tile image
   static constexpr uint32_t A_BYTES = H == 64 ? 2 * TILE : TILE;  // H = 64: zero pad block for M = 128 dW
   static constexpr uint32_t W_LAYER = H * H * 2u;
@@ -84,11 +85,13 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
   float *sMu = sHsum + 2 * 4 * (H + 4);  // [2 tiles][128 rows][2 halves]
   float *sU = sMu + 2 * 128 * 2;         // [8] upstream u per 32-sample chunk of the group
   float *sP = sU + 64;                   // [8] chunk sums of M
-  float *sMisc = sP + 64;                // loss partials
+  float *sMisc = sP + 64;                // [16] loss partials per warp
+  float *sWq = sMisc + 16;               // [<= 8] quadrature weights of the group's rays (N_s >= 32)
+  float *sY = sMisc + 24;                // [<= 8] measured data of the group's pixels
   uint64_t *bars = reinterpret_cast<uint64_t *>(sMisc + 64);
   uint64_t *a_full = bars, *acc_full = bars + 2, *sa_free = bars + 4;  // [2] each
-  uint64_t *w_bar = bars + 6, *xb_bar = bars + 7;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 8);
+  uint64_t *w_bar = bars + 6, *xb_bar = bars + 7, *xb_free = bars + 8;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 9);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (warp == 0) {
@@ -99,10 +102,11 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
     for (int s = 0; s < 2; ++s) {
       mbar_init(&a_full[s], kF2TileArrivals);
       mbar_init(&acc_full[s], 1);
-      mbar_init(&sa_free[s], 1);
+      mbar_init(&sa_free[s], 2);  // MMA retired (tcgen05.commit) + bulk store done reading (copy warp)
     }
     mbar_init(w_bar, 1);
     mbar_init(xb_bar, 1);
+    mbar_init(xb_free, 1);
     fence_mbar_init();
   }
   const int64_t per = (int64_t)H * H + H;
@@ -141,56 +145,25 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
   const uint64_t pol_keep = policy_evict_last(), pol_stream = policy_evict_first();
 
   if (tid >= EPI) {
-    // ===================================================== MMA issuer / copy engine
-    if (lane == 0) {
+    const uint8_t *wsrc = reinterpret_cast<const uint8_t *>(p.wpack_half);
+    if (warp == EPI / 32 && lane == 0) {
+      // ===================================================== MMA issuer (never blocks on copies)
       const uint32_t idf = idesc_bf16(128, H, 0, 0), idb = idesc_bf16(128, H, 0, 1), idw = idesc_bf16(128, H, 1, 1);
-      const uint8_t *wsrc = reinterpret_cast<const uint8_t *>(p.wpack_half);
-      if (L > 1) {
-        const uint32_t rb = (uint32_t)(L - 1) * LY::W_LAYER;
-        mbar_arrive_expect_tx(w_bar, rb);
-        for (uint32_t off = 0; off < rb; off += 32768u)
-          bulk_g2s(sW + off, wsrc + LY::W_LAYER + off, min(32768u, rb - off), w_bar);
-        mbar_wait(w_bar, 0);
-      }
-      uint32_t xph = 0;
-      auto xb_load = [&](const void *src, uint32_t bytes, uint64_t pol) {
-        mbar_arrive_expect_tx(xb_bar, bytes);
-        for (uint32_t off = 0; off < bytes; off += 32768u)
-          bulk_g2s_hint(sXB + off, reinterpret_cast<const uint8_t *>(src) + off, min(32768u, bytes - off), xb_bar, pol);
-      };
+      if (L > 1) mbar_wait(w_bar, 0);
+      uint32_t aph[2] = {0, 0}, xph = 0, dw_init = 0;
       auto xb_wait = [&]() {
         mbar_wait(xb_bar, xph);
         xph ^= 1;
+        tc_fence_after();
       };
-      xb_load(wsrc, LY::W_LAYER, pol_keep);  // W_0 for the first group's forward
-      bool xb_is_w0 = true, xb_pending = true;
-      uint32_t aph[2] = {0, 0}, ncommit[2] = {0, 0}, dw_init = 0;
-      auto commit = [&](int s) {
-        umma_commit(&acc_full[s]);
-        ++ncommit[s];
-      };
-      auto wait_commit = [&](int s) { mbar_wait(&acc_full[s], (ncommit[s] - 1) & 1); };
       for (int64_t gi = blockIdx.x; gi < n_groups; gi += gridDim.x) {
-        const bool more = gi + (int64_t)gridDim.x < n_groups;
-        // ---------------------------------------------------------------- forward
-        for (int l = 0; l < L; ++l) {
+        for (int l = 0; l < L; ++l)
           for (int s = 0; s < 2; ++s) {
-            const int64_t tile = 2 * gi + s;
             const uint32_t a_base = a0_base + s * LY::A_BYTES;
             mbar_wait(&a_full[s], aph[s]);
             aph[s] ^= 1;
             tc_fence_after();
-            if (l >= nu)
-              bulk_s2g_hint(ring_h(s, l - nu), sA0 + s * LY::A_BYTES, TILE, pol_keep);
-            else if (l > 0)  // layer 0's input (the GRFF features) is recomputed by the dW GEMM
-              bulk_s2g_hint(p.hstash + ((size_t)l * p.n_tiles + tile) * TILE, sA0 + s * LY::A_BYTES, TILE,
-                            pol_stream);
-            bulk_commit();
-            if (l == 0 && xb_pending) {
-              xb_wait();
-              xb_pending = false;
-              tc_fence_after();
-            }
+            if (l == 0 && s == 0) xb_wait();  // W_0 of this group
             const uint32_t wl = l == 0 ? xb_base : w_base + (uint32_t)(l - 1) * LY::W_LAYER;
             umma_bf16(tmem + s * H, sdesc_none(ones_base, 128, 256), sdesc_none(biasb_base + l * LY::BIAS_B, 128, 256),
                       idf, 0u);
@@ -198,34 +171,19 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
             for (int kk = 0; kk < H / 16; ++kk)
               umma_bf16(tmem + s * H, sdesc_sw128(a_base + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
                         sdesc_sw128(wl + (kk >> 2) * (H * 128) + (kk & 3) * 32, 16, 1024), idf, 1u);
-            commit(s);
-            bulk_wait_read_all();
-            mbar_arrive(&sa_free[s]);
+            umma_commit(&acc_full[s]);
+            umma_commit(&sa_free[s]);
+            if (l == 0 && s == 1) umma_commit(xb_free);  // W_0 retired for this group
           }
-        }
-        // XB: W_0 -> h_{L-1}(tile 0) once every forward MMA of the group has retired
-        wait_commit(0);
-        wait_commit(1);
-        xb_is_w0 = false;
-        // ---------------------------------------------------------------- backward
-        // (the loss runs on the epilogue warps in between)
-        bool first_fused = true;
-        for (int l = L - 1; l >= 0; --l) {
+        for (int l = L - 1; l >= 0; --l)
           for (int s = 0; s < 2; ++s) {
-            const int64_t tile = 2 * gi + s;
             const uint32_t a_base = a0_base + s * LY::A_BYTES;
             const bool fused = l >= nu;
-            if (fused && first_fused) {
-              xb_load(ring_h(s, l - nu), TILE, pol_stream);
-              first_fused = false;
-            }
             mbar_wait(&a_full[s], aph[s]);
             aph[s] ^= 1;
             tc_fence_after();
-            bool st = false;
             if (fused) {
-              xb_wait();
-              tc_fence_after();
+              xb_wait();  // XB = h_{l-1} of this tile
               const uint32_t dwt = tmem + (uint32_t)(2 * H + (l - nu) * H);
               const uint32_t seen = (dw_init >> (l - nu)) & 1u;  // TMEM is not zeroed: first MMA overwrites
               dw_init |= 1u << (l - nu);
@@ -233,10 +191,6 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
               for (int kk = 0; kk < 8; ++kk)
                 umma_bf16(dwt, sdesc_sw128(a_base + kk * 2048, 16384, 1024), sdesc_sw128(xb_base + kk * 2048, 16384, 1024),
                           idw, (seen || kk > 0) ? 1u : 0u);
-            } else {
-              bulk_s2g_hint(p.dstash + ((size_t)l * p.n_tiles + tile) * TILE, sA0 + s * LY::A_BYTES, TILE, pol_stream);
-              bulk_commit();
-              st = true;
             }
             if (l > 0) {
               const uint32_t wl = w_base + (uint32_t)(l - 1) * LY::W_LAYER;
@@ -245,26 +199,84 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
                 umma_bf16(tmem + s * H, sdesc_sw128(a_base + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
                           sdesc_sw128(wl + kk * 2048, H * 128, 1024), idb, kk > 0);
             }
-            commit(s);
-            if (st) bulk_wait_read_all();
+            umma_commit(&acc_full[s]);
+            umma_commit(&sa_free[s]);
+            if (fused) umma_commit(xb_free);
+          }
+      }
+    } else if (warp == EPI / 32 + 1 && lane == 0) {
+      // ===================================================== copy engine: weights, XB, ring / stash stores
+      if (L > 1) {
+        const uint32_t rb = (uint32_t)(L - 1) * LY::W_LAYER;
+        mbar_arrive_expect_tx(w_bar, rb);
+        for (uint32_t off = 0; off < rb; off += 32768u)
+          bulk_g2s(sW + off, wsrc + LY::W_LAYER + off, min(32768u, rb - off), w_bar);
+      }
+      auto xb_load = [&](const void *src, uint32_t bytes, uint64_t pol) {
+        mbar_arrive_expect_tx(xb_bar, bytes);
+        for (uint32_t off = 0; off < bytes; off += 32768u)
+          bulk_g2s_hint(sXB + off, reinterpret_cast<const uint8_t *>(src) + off, min(32768u, bytes - off), xb_bar, pol);
+      };
+      xb_load(wsrc, LY::W_LAYER, pol_keep);  // W_0 for the first group's forward
+      uint32_t aph[2] = {0, 0}, fph = 0;
+      auto free_wait = [&]() {
+        mbar_wait(xb_free, fph);
+        fph ^= 1;
+      };
+      for (int64_t gi = blockIdx.x; gi < n_groups; gi += gridDim.x) {
+        const bool more = gi + (int64_t)gridDim.x < n_groups;
+        // ---------------------------------------------------------------- forward
+        for (int l = 0; l < L; ++l)
+          for (int s = 0; s < 2; ++s) {
+            const int64_t tile = 2 * gi + s;
+            uint8_t *sA = sA0 + s * LY::A_BYTES;
+            mbar_wait(&a_full[s], aph[s]);
+            aph[s] ^= 1;
+            if (l == L - 1 && s == 0 && l >= nu) {
+              // the top layer's input of stream 0 is the first dW operand of the backward: into
+              // XB as soon as W_0 has retired
+              free_wait();
+              bulk_s2g_hint(ring_h(0, l - nu), sA, TILE, pol_keep);
+              bulk_commit();
+              bulk_wait_all();
+              xb_load(ring_h(0, l - nu), TILE, pol_stream);
+            } else if (l >= nu) {
+              bulk_s2g_hint(ring_h(s, l - nu), sA, TILE, pol_keep);
+              bulk_commit();
+              bulk_wait_read_all();
+            } else if (l > 0) {  // layer 0's input (the GRFF features) is recomputed by the dW GEMM
+              bulk_s2g_hint(p.hstash + ((size_t)l * p.n_tiles + tile) * TILE, sA, TILE, pol_stream);
+              bulk_commit();
+              bulk_wait_read_all();
+            }
             mbar_arrive(&sa_free[s]);
-            if (fused) {
-              // XB is reused: wait until this dW MMA has retired, then load the next operand
-              wait_commit(s);
+          }
+        // ---------------------------------------------------------------- backward
+        for (int l = L - 1; l >= 0; --l)
+          for (int s = 0; s < 2; ++s) {
+            const int64_t tile = 2 * gi + s;
+            uint8_t *sA = sA0 + s * LY::A_BYTES;
+            const bool fused = l >= nu;
+            mbar_wait(&a_full[s], aph[s]);
+            aph[s] ^= 1;
+            if (!fused) {
+              bulk_s2g_hint(p.dstash + ((size_t)l * p.n_tiles + tile) * TILE, sA, TILE, pol_stream);
+              bulk_commit();
+              bulk_wait_read_all();
+            }
+            mbar_arrive(&sa_free[s]);
+            if (fused) {  // next XB content, once this dW has retired
               const int ns = s == 0 ? 1 : 0, nl = s == 0 ? l : l - 1;
+              free_wait();
               if (nl >= nu) {
+                bulk_wait_all();  // the ring image was written by this thread's bulk store
                 xb_load(ring_h(ns, nl - nu), TILE, pol_stream);
               } else if (more) {
                 xb_load(wsrc, LY::W_LAYER, pol_keep);  // W_0 for the next group's forward
-                xb_is_w0 = true;
-                xb_pending = true;
               }
             }
           }
-        }
       }
-      (void)xb_is_w0;
-      if (xb_pending) xb_wait();
       bulk_wait_all();
     }
     __syncwarp();
@@ -325,6 +337,17 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
       const int64_t tile = 2 * gi + s;
       const int64_t g = tile * 128 + row;
       const bool valid = g < p.nsamp;
+      // loss operands of the group's pixels (quadrature weights, measured data), fetched now so
+      // that the loss phase -- where both streams wait -- has no global-memory latency
+      float wq_pre = 0.f, y_pre = 0.f;  // loads in flight during the feature computation
+      if (tid < pix_per_group * p.S) {
+        const int64_t ray = gi * pix_per_group * p.S + tid;
+        if (ray < p.n_pix * p.S) wq_pre = p.rec32[2 * ray + 1].w;
+      }
+      if (tid < pix_per_group) {
+        const int64_t pix = gi * pix_per_group + tid;
+        if (pix < p.n_pix) y_pre = p.y[pix];
+      }
       // ------------------------------------------------------------ a5/a6 features
       {
         const float4 rb = grff_coords(p.rec32, g, p.lg_ns, p.n_s, valid, p.jit);
@@ -341,6 +364,8 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
         }
       }
       fence_proxy_async_smem();
+      if (tid < pix_per_group * p.S) sWq[tid] = wq_pre;
+      if (tid < pix_per_group) sY[tid] = y_pre;
       PH2(0);
       f2_arrive_tile(&a_full[s]);
       // ------------------------------------------------------------ a7/a8 forward layers
@@ -464,8 +489,7 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
           float pv[8], wqv[8];
           for (int ss = 0; ss < p.S; ++ss) {
             const int ray_l = tid * p.S + ss;
-            const int64_t ray = pix * p.S + ss;
-            wqv[ss] = p.rec32[2 * ray + 1].w;
+            wqv[ss] = sWq[ray_l];  // prefetched at the start of the group
             float acc = 0.f;
             for (int c = 0; c < chunks_per_ray; ++c) acc += sP[ray_l * chunks_per_ray + c];
             pv[ss] = wqv[ss] > 0.f ? wqv[ss] * acc : 0.f;
@@ -484,7 +508,7 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
             fh = m - logf(T);
           }
           if (p.fhat) p.fhat[pix] = fh;
-          const float res = p.y[pix] - fh;
+          const float res = sY[tid] - fh;
           loss_acc += res * res;
           const float gg = -2.f * res * p.inv_n;
           for (int ss = 0; ss < p.S; ++ss) {
