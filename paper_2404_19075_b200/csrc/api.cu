@@ -616,7 +616,7 @@ dinr_status step_grad(dinr_ctx *c, const int64_t *idx, int64_t n, const float *y
       if (s) return s;
     }
     Launch L_(c, T_ASM, st);
-    k_assemble2<<<(unsigned)((c->P + 1 + 255) / 256), 256, 0, st>>>(
+    k_assemble2<<<(unsigned)((c->P + 1 + 31) / 32), 256, 0, st>>>(
         c->H, c->L, c->P, pl.nu, pl.ksplit, pl.dw_part, pl.db_part, pl.grid_f, pl.dwf, pl.dbf, pl.head_part,
         pl.grid_f, pl.loss_part, pl.grid_f, 1.f / (float)n, accumulate, grad);
     CUDA_TRY(c, cudaGetLastError());

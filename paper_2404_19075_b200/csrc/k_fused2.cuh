@@ -30,6 +30,14 @@ __device__ __forceinline__ void f2_wait(uint64_t *bar, uint32_t parity) {
   else
     mbar_wait(bar, parity);
 }
+// waits of the MMA-issuer / copy warps: suspended try_wait (DINR_F2_CTL_SPIN: plain spinning)
+__device__ __forceinline__ void f2_ctl_wait(uint64_t *bar, uint32_t parity) {
+#ifdef DINR_F2_CTL_SPIN
+  mbar_wait(bar, parity);
+#else
+  mbar_wait_sleep(bar, parity, 1000);
+#endif
+}
 // operand-tile handoff: one arrival per warp after the warp's generic-proxy smem writes are fenced
 __device__ __forceinline__ void f2_arrive_tile(uint64_t *bar) {
 #ifdef DINR_F2_THREAD_ARRIVE
@@ -149,10 +157,10 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
     if (warp == EPI / 32 && lane == 0) {
       // ===================================================== MMA issuer (never blocks on copies)
       const uint32_t idf = idesc_bf16(128, H, 0, 0), idb = idesc_bf16(128, H, 0, 1), idw = idesc_bf16(128, H, 1, 1);
-      if (L > 1) mbar_wait(w_bar, 0);
+      if (L > 1) f2_ctl_wait(w_bar, 0);
       uint32_t aph[2] = {0, 0}, xph = 0, dw_init = 0;
       auto xb_wait = [&]() {
-        mbar_wait(xb_bar, xph);
+        f2_ctl_wait(xb_bar, xph);
         xph ^= 1;
         tc_fence_after();
       };
@@ -160,7 +168,7 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
         for (int l = 0; l < L; ++l)
           for (int s = 0; s < 2; ++s) {
             const uint32_t a_base = a0_base + s * LY::A_BYTES;
-            mbar_wait(&a_full[s], aph[s]);
+            f2_ctl_wait(&a_full[s], aph[s]);
             aph[s] ^= 1;
             tc_fence_after();
             if (l == 0 && s == 0) xb_wait();  // W_0 of this group
@@ -179,7 +187,7 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
           for (int s = 0; s < 2; ++s) {
             const uint32_t a_base = a0_base + s * LY::A_BYTES;
             const bool fused = l >= nu;
-            mbar_wait(&a_full[s], aph[s]);
+            f2_ctl_wait(&a_full[s], aph[s]);
             aph[s] ^= 1;
             tc_fence_after();
             if (fused) {
@@ -220,7 +228,7 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
       xb_load(wsrc, LY::W_LAYER, pol_keep);  // W_0 for the first group's forward
       uint32_t aph[2] = {0, 0}, fph = 0;
       auto free_wait = [&]() {
-        mbar_wait(xb_free, fph);
+        f2_ctl_wait(xb_free, fph);
         fph ^= 1;
       };
       for (int64_t gi = blockIdx.x; gi < n_groups; gi += gridDim.x) {
@@ -230,7 +238,7 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
           for (int s = 0; s < 2; ++s) {
             const int64_t tile = 2 * gi + s;
             uint8_t *sA = sA0 + s * LY::A_BYTES;
-            mbar_wait(&a_full[s], aph[s]);
+            f2_ctl_wait(&a_full[s], aph[s]);
             aph[s] ^= 1;
             if (l == L - 1 && s == 0 && l >= nu) {
               // the top layer's input of stream 0 is the first dW operand of the backward: into
@@ -257,7 +265,7 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
             const int64_t tile = 2 * gi + s;
             uint8_t *sA = sA0 + s * LY::A_BYTES;
             const bool fused = l >= nu;
-            mbar_wait(&a_full[s], aph[s]);
+            f2_ctl_wait(&a_full[s], aph[s]);
             aph[s] ^= 1;
             if (!fused) {
               bulk_s2g_hint(p.dstash + ((size_t)l * p.n_tiles + tile) * TILE, sA, TILE, pol_stream);

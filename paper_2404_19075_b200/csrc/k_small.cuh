@@ -166,38 +166,54 @@ __global__ void k_adam_pack(float *__restrict__ params, const float *__restrict_
 // Assembly for the fused path (H <= 128): layers [0, nu) from the dW GEMM partials
 // ([l][ks5][128][H]), layers [nu, L) from the fused kernel's per-CTA TMEM partials
 // ([l - nu][ksf][128][H]); fixed summation order -> deterministic.
-__global__ void k_assemble2(int H, int L, int64_t P, int nu, int ks5, const float *__restrict__ dw5,
-                            const float *__restrict__ db5, int ksf, const float *__restrict__ dwf,
-                            const float *__restrict__ dbf, const float *__restrict__ head_part, int nhead,
-                            const float *__restrict__ loss_part, int nloss, float inv_n, int accumulate,
-                            float *__restrict__ grad) {
-  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (q > P) return;
+// Gradient assembly for the fused path: parameter q sums its per-CTA / per-K-split partials.
+// Block = 32 consecutive parameters (lanes, coalesced) x 8 warps; warp w sums partials w, w+8,
+// ... and the 8 warp sums are added in fixed order (deterministic).
+__global__ void __launch_bounds__(256) k_assemble2(int H, int L, int64_t P, int nu, int ks5,
+                                                   const float *__restrict__ dw5, const float *__restrict__ db5, int ksf,
+                                                   const float *__restrict__ dwf, const float *__restrict__ dbf,
+                                                   const float *__restrict__ head_part, int nhead,
+                                                   const float *__restrict__ loss_part, int nloss, float inv_n,
+                                                   int accumulate, float *__restrict__ grad) {
+  __shared__ float red[8][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t q = (int64_t)blockIdx.x * 32 + lane;
+  const int64_t per = (int64_t)H * H + H;
   float v = 0.f;
-  int64_t per = (int64_t)H * H + H;
   if (q == P) {
-    for (int b = 0; b < nloss; ++b) v += loss_part[b];
-    v *= inv_n;
+    for (int b = w; b < nloss; b += 8) v += loss_part[b];
   } else if (q < (int64_t)L * per) {
-    int l = (int)(q / per);
-    int64_t e = q - (int64_t)l * per;
+    const int l = (int)(q / per);
+    const int64_t e = q - (int64_t)l * per;
     const bool f = l >= nu;
     const int ks = f ? ksf : ks5;
     const int ll = f ? l - nu : l;
+    const float *src;
+    size_t stride;
     if (e < (int64_t)H * H) {
-      int o = (int)(e / H), i = (int)(e % H);
-      const float *src = (f ? dwf : dw5) + ((size_t)ll * ks * 128 + o) * H + i;
-      for (int s = 0; s < ks; ++s) v += src[(size_t)s * 128 * H];
+      const int o = (int)(e / H), i = (int)(e % H);
+      src = (f ? dwf : dw5) + ((size_t)ll * ks * 128 + o) * H + i;
+      stride = (size_t)128 * H;
     } else {
-      int o = (int)(e - (int64_t)H * H);
-      const float *src = (f ? dbf : db5) + (size_t)ll * ks * 128 + o;
-      for (int s = 0; s < ks; ++s) v += src[(size_t)s * 128];
+      src = (f ? dbf : db5) + (size_t)ll * ks * 128 + (e - (int64_t)H * H);
+      stride = 128;
     }
-  } else {
-    int k = (int)(q - (int64_t)L * per);
-    for (int b = 0; b < nhead; ++b) v += head_part[(int64_t)b * (H + 1) + k];
+#pragma unroll 4
+    for (int s = w; s < ks; s += 8) v += src[(size_t)s * stride];
+  } else if (q < P) {
+    const int k = (int)(q - (int64_t)L * per);
+#pragma unroll 4
+    for (int b = w; b < nhead; b += 8) v += head_part[(int64_t)b * (H + 1) + k];
   }
-  grad[q] = accumulate ? grad[q] + v : v;
+  red[w][lane] = v;
+  __syncthreads();
+  if (w == 0 && q <= P) {
+    float t = 0.f;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) t += red[j][lane];
+    if (q == P) t *= inv_n;
+    grad[q] = accumulate ? grad[q] + t : t;
+  }
 }
 
 }  // namespace dinr
