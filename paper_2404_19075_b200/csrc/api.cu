@@ -22,6 +22,7 @@
 #include "k_tc_mlp.cuh"
 #include "k_fused.cuh"
 #include "k_fused2.cuh"
+#include "k_dw01.cuh"
 #include "k_infer.cuh"
 #include "k_phantom.cuh"
 #include "nccl_dl.cuh"
@@ -102,6 +103,7 @@ struct Plan {
   int nloss;
   // fused training path (k_fused): nf top layers' dW in TMEM, nu = L - nf through K5
   bool fused, fused2;  // fused2: two concurrent tile streams (k_fused2)
+  bool dw01;           // layers 0 and 1 unfused, both inputs recomputed by k_dw01 (no input stash)
   int nf, nu, grid_f, dw_layers;
   uint8_t *ring;
   float *dwf, *dbf;
@@ -173,6 +175,7 @@ size_t plan_layout(dinr_ctx *c, int64_t n, bool train, bool host_io, Plan &pl, v
   }
   pl.fused = train && use_fused(c);
   pl.fused2 = pl.fused && use_fused2(c);
+  pl.dw01 = false;
   pl.nf = pl.nu = pl.grid_f = 0;
   pl.dw_layers = L;
   pl.ring = nullptr;
@@ -185,7 +188,11 @@ size_t plan_layout(dinr_ctx *c, int64_t n, bool train, bool host_io, Plan &pl, v
     pl.grid_f = (int)std::max<int64_t>(1, std::min<int64_t>(n_groups, c->sm_count));
     // dW GEMM grid: layer 0 recomputes its input (GRFF features) and gets w0 x the CTAs of a
     // layer that streams both operands from HBM
-    if (pl.nu > 0) {
+    static const bool no_dw01 = std::getenv("DINR_NO_DW01") != nullptr;
+    pl.dw01 = pl.fused2 && pl.nu == 2 && H == 128 && !no_dw01;
+    if (pl.dw01) {
+      pl.ks0 = pl.ks1 = pl.ksplit = (int)std::min<int64_t>(c->sm_count, pl.n_tiles);
+    } else if (pl.nu > 0) {
       static const double w0 = std::getenv("DINR_DW_W0") ? std::atof(std::getenv("DINR_DW_W0")) : 2.0;
       const int sm = c->sm_count;
       pl.ks0 = pl.nu == 1 ? sm : std::max(1, (int)(sm * w0 / (w0 + pl.nu - 1) + 0.5));
@@ -390,6 +397,7 @@ dinr_status launch_fused(dinr_ctx *c, const Plan &pl, const float *y, cudaStream
   p.y = y;
   p.fhat = pl.fhat;
   p.ring = pl.ring;
+  p.dw01 = pl.dw01 ? 1 : 0;
   p.hstash = pl.hstash;
   p.dstash = pl.dstash;
   p.n_tiles = pl.n_tiles;
@@ -455,7 +463,32 @@ dinr_status tc_forward(dinr_ctx *c, const Plan &pl, bool train, cudaStream_t st)
   return fail(c, DINR_EINVAL, "unsupported width");
 }
 
+dinr_status launch_dw01(dinr_ctx *c, const Plan &pl, cudaStream_t st) {
+  Dw01Params p{};
+  p.dstash = pl.dstash;
+  p.n_tiles = pl.n_tiles;
+  p.nsamp = pl.nsamp;
+  p.rec32 = pl.rec32;
+  p.jit = pl.jit;
+  p.B = c->d_B;
+  p.n_s = c->geom.samples_per_ray;
+  p.lg_ns = 0;
+  while ((1 << p.lg_ns) < p.n_s) ++p.lg_ns;
+  p.params = c->d_params;
+  p.wpack_half = c->d_wpack_half;
+  p.dw_part = pl.dw_part;
+  p.db_part = pl.db_part;
+  const size_t smem = Dw01Layout<128>::smem_bytes();
+  dinr_status s = set_smem(c, k_dw01<128>, smem);
+  if (s) return s;
+  Launch L_(c, T_DW, st);
+  k_dw01<128><<<pl.ksplit, Dw01Layout<128>::NT, smem, st>>>(p);
+  CUDA_TRY(c, cudaGetLastError());
+  return DINR_OK;
+}
+
 dinr_status tc_dw(dinr_ctx *c, const Plan &pl, cudaStream_t st) {
+  if (pl.dw01) return launch_dw01(c, pl, st);
   switch (c->H) {
     case 64: return launch_tc_dw<64>(c, pl, st);
     case 128: return launch_tc_dw<128>(c, pl, st);

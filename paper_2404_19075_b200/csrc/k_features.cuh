@@ -27,6 +27,36 @@ __device__ __forceinline__ float4 grff_coords(const float4 *__restrict__ rec32, 
   return r;
 }
 
+// The same coordinates split into a load (issued early, e.g. one tile ahead) and the arithmetic.
+struct RayRec {
+  float4 a, b;
+};
+__device__ __forceinline__ RayRec grff_fetch(const float4 *__restrict__ rec32, int64_t g, int lg_ns, bool valid) {
+  RayRec r;
+  if (valid) {
+    const int64_t ray = g >> lg_ns;
+    r.a = rec32[2 * ray];
+    r.b = rec32[2 * ray + 1];
+  } else {
+    r.a = r.b = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  return r;
+}
+__device__ __forceinline__ float4 grff_coords_from(const RayRec &rr, int64_t g, int lg_ns, int n_s, bool valid,
+                                                   const Jitter &jt) {
+  float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (valid) {
+    const int64_t ray = g >> lg_ns;
+    const uint32_t j = (uint32_t)(g & (n_s - 1));
+    const float jj = (float)j + sample_offset(jt, ray, j);
+    r.x = rr.a.w;
+    r.y = rr.a.z + jj * rr.b.z;
+    r.z = rr.a.y + jj * rr.b.y;
+    r.w = rr.a.x + jj * rr.b.x;
+  }
+  return r;
+}
+
 // Frequencies c0 .. c0+7 (B rows as float4 in shared memory): packed bf16 cos / sin pairs.
 __device__ __forceinline__ void grff8(const float4 *sB4, int c0, float4 rb, uint32_t (&pc)[4], uint32_t (&ps)[4]) {
 #pragma unroll

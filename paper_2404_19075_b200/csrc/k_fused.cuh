@@ -39,6 +39,7 @@ struct FusedParams {
   float *head_part;       // [grid][H+1]
   float *loss_part;       // [grid]
   Jitter jit;                // N3 sample placement
+  int dw01;                  // layer 1's input is recomputed after the kernel (k_dw01): no h stash
   unsigned long long *dbg;  // DINR_PHASES builds: [grid][8] cycle counters
 };
 

@@ -77,6 +77,11 @@ __device__ __forceinline__ void bulk_wait_read_all() {
 }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
+// Prefetch a global range into L2 (no shared-memory destination, no completion tracking).
+__device__ __forceinline__ void bulk_prefetch_l2(const void *gsrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(gsrc), "r"(bytes) : "memory");
+}
+
 // L2 cache policies (createpolicy) and hinted variants of the copies / accesses above.
 __device__ __forceinline__ uint64_t policy_evict_last() {
   uint64_t p;
