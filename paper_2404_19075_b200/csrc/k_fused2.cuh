@@ -425,11 +425,9 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
             // columns (acc[s] is idle until the first backward dX MMA)
             tmem_st8(trow + hc * 8, s2k);
           } else {
-            uint4 *s2dst = reinterpret_cast<uint4 *>(ring_s2(s, l));
-#pragma unroll
-            for (int q = 0; q < 2; ++q)
-              st_global_v4_hint(s2dst + (size_t)((col0 >> 3) + q) * 128 + row,
-                                make_uint4(s2k[4 * q], s2k[4 * q + 1], s2k[4 * q + 2], s2k[4 * q + 3]), pol_keep);
+            // ring layout [16-column chunk][row][32 B]: one 256-bit store per thread, a warp covers
+            // 1 KB contiguous
+            st_global_v8_hint(ring_s2(s, l) + ((size_t)(col0 >> 4) * 128 + row) * 32, s2k, pol_keep);
           }
           if (!last) {
             if (hc == 0) wait_sa();
@@ -608,10 +606,9 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
 #pragma unroll
           for (int c = 0; c < NCH; ++c)
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
-              sq[c][q] = ld_global_v4_hint(reinterpret_cast<const uint4 *>(ring_s2(s, l - 1)) +
-                                               (size_t)(((ch * (H / 2) + c * 32) >> 3) + q) * 128 + row,
-                                           pol_stream);
+            for (int hf = 0; hf < 2; ++hf)
+              ld_global_v8_hint(ring_s2(s, l - 1) + ((size_t)((ch * (H / 2) + c * 32 + hf * 16) >> 4) * 128 + row) * 32,
+                                sq[c][2 * hf], sq[c][2 * hf + 1], pol_stream);
         }
         if (l >= nu) {  // db of a fused layer: column sums of delta over the warp's 32 rows
 #pragma unroll

@@ -111,6 +111,17 @@ __device__ __forceinline__ void st_global_v4_hint(void *p, uint4 v, uint64_t pol
                "r"(v.w), "l"(pol)
                : "memory");
 }
+// 32-byte vector store / load (sm_100: STG/LDG .256) with an L2 cache policy.
+__device__ __forceinline__ void st_global_v8_hint(void *p, const uint32_t (&v)[8], uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8}, %9;" ::"l"(p), "r"(v[0]),
+               "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void ld_global_v8_hint(const void *p, uint4 &a, uint4 &b, uint64_t pol) {
+  asm volatile("ld.global.L2::cache_hint.v8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8], %9;"
+               : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
+               : "l"(p), "l"(pol));
+}
 __device__ __forceinline__ uint4 ld_global_v4_hint(const void *p, uint64_t pol) {
   uint4 v;
   asm volatile("ld.global.L2::cache_hint.v4.b32 {%0, %1, %2, %3}, [%4], %5;"
@@ -121,6 +132,13 @@ __device__ __forceinline__ uint4 ld_global_v4_hint(const void *p, uint64_t pol) 
 
 __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
+
+__device__ __forceinline__ uint4 ld_shared_v4(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr)
+               : "memory");
+  return v;
 }
 
 // Make generic-proxy shared-memory writes visible to the async proxy (tensor core, TMA).
