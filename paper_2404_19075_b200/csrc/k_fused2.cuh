@@ -410,11 +410,7 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
               const uint32_t yb = pack_bf16x2(__uint_as_float(cur[i + 2 * e]), __uint_as_float(cur[i + 2 * e + 1]));
-#ifdef DINR_EXP_NO_TANH
-              const uint32_t t = yb ^ 0x00400040u;
-#else
               const uint32_t t = bf2_tanh(yb);
-#endif
               hpk[i / 2 + e] = bf2_fma(yb, t, yb);
               const uint32_t w = bf2_fma(t, t ^ kBf2Sign, kBf2One);
               s2k[i / 2 + e] = bf2_fma(yb, w, bf2_add(t, kBf2One));
@@ -431,12 +427,8 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
           }
           if (!last) {
             if (hc == 0) wait_sa();
-#ifndef DINR_EXP_NO_STS
 #pragma unroll
             for (int q = 0; q < 2; ++q)
-#else
-            for (int q = 0; q < 2 && l == 99; ++q)
-#endif
               st_shared_v4(a_base + aoff[hc >> 1][(hc & 1) * 2 + q], hpk[4 * q], hpk[4 * q + 1], hpk[4 * q + 2],
                            hpk[4 * q + 3]);
           } else {
@@ -613,14 +605,29 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
         if (l >= nu) {  // db of a fused layer: column sums of delta over the warp's 32 rows
 #pragma unroll
           for (int c = 0; c < NCH; ++c) {
-            float d[32];
+            // transpose-reduce: the first two butterfly levels on packed bf16 pairs (sums of 2
+            // and 4 rows), the last three in fp32; lane l ends with column l's 32-row sum
+            uint32_t w[16];
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              d[2 * i] = bf16lo(dp[c][i]);
-              d[2 * i + 1] = bf16hi(dp[c][i]);
+            for (int i = 0; i < 16; ++i) w[i] = dp[c][i];
+#pragma unroll
+            for (int o = 8; o >= 4; o >>= 1) {  // lane bits 16, 8 <-> packed words 8, 4 apart
+              const bool up = (lane & (2 * o)) != 0;
+#pragma unroll
+              for (int i = 0; i < o; ++i) {
+                const uint32_t send = up ? w[i] : w[i + o];
+                const uint32_t keep = up ? w[i + o] : w[i];
+                w[i] = bf2_add(keep, (uint32_t)__shfl_xor_sync(0xffffffffu, (int)send, 2 * o));
+              }
+            }
+            float d[8];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              d[2 * i] = bf16lo(w[i]);
+              d[2 * i + 1] = bf16hi(w[i]);
             }
 #pragma unroll
-            for (int o = 16; o >= 1; o >>= 1) {
+            for (int o = 4; o >= 1; o >>= 1) {
               const bool up = (lane & o) != 0;
 #pragma unroll
               for (int i = 0; i < o; ++i) {
