@@ -440,9 +440,27 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
             }
 #pragma unroll
             for (int i = 0; i < 16; ++i) mu_part = fmaf(sWo[col0 + i], hv[i], mu_part);
-            // column sums over the warp's 32 rows: lanes l and l^16 end with column (l & 15)
+            // column sums over the warp's 32 rows (lanes l and l^16 end with column l & 15): two
+            // butterfly levels on packed bf16 pairs, then fp32
+            uint32_t hw[8];
 #pragma unroll
-            for (int o = 8; o >= 1; o >>= 1) {
+            for (int i = 0; i < 8; ++i) hw[i] = hpk[i];
+#pragma unroll
+            for (int o = 4; o >= 2; o >>= 1) {  // lane bits 8, 4 <-> packed words 4, 2 apart
+              const bool up = (lane & (2 * o)) != 0;
+#pragma unroll
+              for (int i = 0; i < o; ++i) {
+                const uint32_t send = up ? hw[i] : hw[i + o];
+                const uint32_t keep = up ? hw[i + o] : hw[i];
+                hw[i] = bf2_add(keep, (uint32_t)__shfl_xor_sync(0xffffffffu, (int)send, 2 * o));
+              }
+            }
+            hv[0] = bf16lo(hw[0]);
+            hv[1] = bf16hi(hw[0]);
+            hv[2] = bf16lo(hw[1]);
+            hv[3] = bf16hi(hw[1]);
+#pragma unroll
+            for (int o = 2; o >= 1; o >>= 1) {
               const bool up = (lane & o) != 0;
 #pragma unroll
               for (int i = 0; i < o; ++i) {
