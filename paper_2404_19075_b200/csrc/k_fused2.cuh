@@ -38,19 +38,24 @@ __device__ __forceinline__ void f2_ctl_wait(uint64_t *bar, uint32_t parity) {
   mbar_wait_sleep(bar, parity, 1000);
 #endif
 }
-// operand-tile handoff: one arrival per warp after the warp's generic-proxy smem writes are fenced
-__device__ __forceinline__ void f2_arrive_tile(uint64_t *bar) {
-#ifdef DINR_F2_THREAD_ARRIVE
-  mbar_arrive(bar);
-#else
+// operand-tile handoff after the writers' generic-proxy smem writes are fenced:
+//   default: the stream's 8 warps meet at a named barrier, one thread arrives (one mbarrier event
+//            per handoff: fewer wake-ups of the warps sleeping on mbarriers)
+//   DINR_F2_WARP_ARRIVE: one arrival per warp
+__device__ __forceinline__ void f2_arrive_tile(uint64_t *bar, int stream) {
+#ifdef DINR_F2_WARP_ARRIVE
+  (void)stream;
   __syncwarp();
   if ((threadIdx.x & 31) == 0) mbar_arrive(bar);
+#else
+  asm volatile("bar.sync %0, 256;" ::"r"(2 + stream) : "memory");
+  if ((threadIdx.x & 255) == 0) mbar_arrive(bar);
 #endif
 }
-#ifdef DINR_F2_THREAD_ARRIVE
-constexpr int kF2TileArrivals = 256;
-#else
+#ifdef DINR_F2_WARP_ARRIVE
 constexpr int kF2TileArrivals = 8;
+#else
+constexpr int kF2TileArrivals = 1;
 #endif
 
 
@@ -375,7 +380,7 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
       if (tid < pix_per_group * p.S) sWq[tid] = wq_pre;
       if (tid < pix_per_group) sY[tid] = y_pre;
       PH2(0);
-      f2_arrive_tile(&a_full[s]);
+      f2_arrive_tile(&a_full[s], s);
       // ------------------------------------------------------------ a7/a8 forward layers
       float mu_part = 0.f;
       for (int l = 0; l < L; ++l) {
@@ -483,7 +488,7 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
         tc_fence_before();
         if (!last) {
           fence_proxy_async_smem();
-          f2_arrive_tile(&a_full[s]);
+          f2_arrive_tile(&a_full[s], s);
         }
         PH2(2);
       }
@@ -611,7 +616,7 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
             st_shared_v4(a_base + aoff[c][q], dp[c][4 * q], dp[c][4 * q + 1], dp[c][4 * q + 2], dp[c][4 * q + 3]);
         fence_proxy_async_smem();
         PH2(5);
-        f2_arrive_tile(&a_full[s]);
+        f2_arrive_tile(&a_full[s], s);
         if (l > 0) {  // prefetch s2 of the next backward step
 #pragma unroll
           for (int c = 0; c < NCH; ++c)
