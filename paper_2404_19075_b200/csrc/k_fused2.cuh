@@ -21,7 +21,7 @@
 namespace dinr {
 
 #ifndef DINR_F2_SUSPEND_NS
-#define DINR_F2_SUSPEND_NS 20000
+#define DINR_F2_SUSPEND_NS 0
 #endif
 // epilogue-side waits: suspended try_wait (0 ns hint = plain spinning probe)
 __device__ __forceinline__ void f2_wait(uint64_t *bar, uint32_t parity) {
@@ -72,7 +72,7 @@ struct Fused2Layout {
   static constexpr uint32_t BIAS_B = H * 32;  // no-swizzle [H rows][16] bf16: hi, lo of b_l / 2
   static size_t smem_bytes(int L) {
     return 1024 + 2 * (size_t)A_BYTES + XB + (size_t)(L - 1) * W_LAYER + ONES + (size_t)L * BIAS_B + (H + 4) * 4 +
-           (H / 2) * 16 + 2 * 4 * (H + 4) * 4 + 2 * 128 * 2 * 4 + 3 * 64 * 4 + 256;
+           (H / 2) * 16 + 2 * 4 * (H + 4) * 4 + 3 * 64 * 4 + 256;
   }
 };
 
@@ -95,9 +95,8 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
   float *sWo = reinterpret_cast<float *>(sBiasB + (size_t)L * LY::BIAS_B);  // w_o[H], b_o
   float *sB = sWo + H + 4;                                                       // C x 4
   float *sHsum = sB + C * 4;             // [2 tiles][4 row chunks][H + 4]
-  float *sMu = sHsum + 2 * 4 * (H + 4);  // [2 tiles][128 rows][2 halves]
-  float *sU = sMu + 2 * 128 * 2;         // [8] upstream u per 32-sample chunk of the group
-  float *sP = sU + 64;                   // [8] chunk sums of M
+  float *sU = sHsum + 2 * 4 * (H + 4);   // [8] upstream u per 32-sample chunk of the group
+  float *sP = sU + 64;                   // [8 chunks][2 column halves] partial sums of w_o . h_L
   float *sMisc = sP + 64;                // [16] loss partials per warp
   float *sWq = sMisc + 16;               // [<= 8] quadrature weights of the group's rays (N_s >= 32)
   float *sY = sMisc + 24;                // [<= 8] measured data of the group's pixels
@@ -492,16 +491,12 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
         }
         PH2(2);
       }
-      sMu[(s * 128 + row) * 2 + ch] = valid ? mu_part : 0.f;
       // ------------------------------------------------------------ a9-a11: combine + loss
-      named_sync(1, EPI);
-      if (warp < 8) {  // chunk sums of M = mu0 (w_o . h_L + b_o), warp q <-> 32-sample chunk q
-        const int ss = warp >> 2, rr = (warp & 3) * 32 + lane;
-        const float m = sWo[H] + sMu[(ss * 128 + rr) * 2] + sMu[(ss * 128 + rr) * 2 + 1];
-        float a = ((2 * gi + ss) * 128 + rr < p.nsamp) ? p.mu0 * m : 0.f;
+      {  // 32-row partial sums of w_o . h_L per (chunk = tile s, lane quadrant; column half)
+        float a = valid ? mu_part : 0.f;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-        if (lane == 0) sP[warp] = a;
+        if (lane == 0) sP[(s * 4 + (warp & 3)) * 2 + ch] = a;
       }
       named_sync(1, EPI);
       if (tid < pix_per_group) {
@@ -512,8 +507,11 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
             const int ray_l = tid * p.S + ss;
             wqv[ss] = sWq[ray_l];  // prefetched at the start of the group
             float acc = 0.f;
-            for (int c = 0; c < chunks_per_ray; ++c) acc += sP[ray_l * chunks_per_ray + c];
-            pv[ss] = wqv[ss] > 0.f ? wqv[ss] * acc : 0.f;
+            for (int c = 0; c < chunks_per_ray; ++c) {  // M = mu0 (w_o . h_L + b_o) over the chunk's 32 samples
+              const int q = ray_l * chunks_per_ray + c;
+              acc += sP[2 * q] + sP[2 * q + 1] + 32.f * sWo[H];
+            }
+            pv[ss] = wqv[ss] > 0.f ? wqv[ss] * (p.mu0 * acc) : 0.f;
           }
           float fh, T = 1.f, m = 0.f;
           if (p.combine == DINR_LINEAR) {
