@@ -2,12 +2,11 @@
 // with both layer inputs recomputed on chip instead of stashed in HBM:
 //   dW_0 = sum delta_0^T gamma(x),      db_0 = sum delta_0          (eq:partiald)
 //   dW_1 = sum delta_1^T h_0,           db_1 = sum delta_1,    h_0 = swish(W_0 gamma(x) + b_0)
-// gamma(x) is recomputed from the ray records (same code and rounding as the fused kernel's
-// layer-0 operand), h_0 by one forward MMA with the same 0.5-prescaled bf16 W_0 image, bias MMA
-// step and packed-bf16 Swish, so both operands equal, bit for bit, what the fused kernel used.
-// Only delta_0 and delta_1 come from HBM (the stash written by k_fused2).
-//   warp 0: bulk loads of the delta tiles (3-slot ring); warp 1: MMA issuer;
-//   warps 2..2+4 NQ: thread = (TMEM lane / sample row, column part): features -> F, y -> h_0 tiles.
+// gamma(x) is the fused kernel's own layer-0 operand tile (bulk-stored by its copy warp), h_0 is
+// recomputed by one forward MMA with the same 0.5-prescaled bf16 W_0 image, bias MMA step and
+// packed-bf16 Swish, so it equals, bit for bit, what the fused kernel used; h_0 is never stored.
+//   warp 0: bulk loads (F double-buffered, delta_0 / delta_1 one slot each); warp 1: MMA issuer;
+//   warps 2..2+4 NQ: thread = (TMEM lane / sample row, column part): y -> h_0 tile.
 // TMEM: y [0, H), dW_0 [H, 2H), dW_1 [2H, 3H), db_0 / db_1 at 3H / 3H + 16 (ones-MMA, column 0).
 #pragma once
 #include "internal.cuh"
@@ -18,6 +17,7 @@ namespace dinr {
 
 struct Dw01Params {
   const uint8_t *dstash;  // [nu][n_tiles] SW128 images of delta_l
+  const uint8_t *fstash;  // [n_tiles] SW128 images of gamma(x) (layer 0's input)
   int64_t n_tiles, nsamp;
   const float4 *rec32;
   Jitter jit;
@@ -34,12 +34,12 @@ struct Dw01Layout {
   static constexpr int NFW = 4 * NQ;       // feature / Swish warps
   static constexpr int NT = 64 + 32 * NFW;
   static constexpr uint32_t TILE = H * 256u;
-  static constexpr int NST = 3;  // ring of delta tiles: slot k holds delta_{k % 2} of tile k / 2
+  static constexpr int NST = 2;  // delta slots: slot l holds delta_l of the current tile
   static constexpr uint32_t ONES_K = 128 * 32;  // no-swizzle [128][16]: columns 0, 1 = 1 (bias MMA)
   static constexpr uint32_t BIAS_B = H * 32;
   static constexpr uint32_t ONES_N = 2048;      // SW128 K-major [16 rows][64] of ones (db MMA B operand)
   static size_t smem_bytes() {
-    return 1024 + (size_t)NST * TILE + 2 * TILE + (size_t)H * H * 2 + ONES_K + BIAS_B + ONES_N + (H / 2) * 16 + 256;
+    return 1024 + (size_t)NST * TILE + 3 * TILE + (size_t)H * H * 2 + ONES_K + BIAS_B + ONES_N + (H / 2) * 16 + 256;
   }
 };
 
@@ -52,8 +52,8 @@ __global__ void __launch_bounds__(Dw01Layout<H>::NT, 1) k_dw01(Dw01Params p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t *sD = smem;                          // NST delta tiles
-  uint8_t *sF = sD + LY::NST * TILE;           // gamma(x) tile
-  uint8_t *sH0 = sF + TILE;                    // h_0 tile
+  uint8_t *sF = sD + LY::NST * TILE;           // gamma(x) tiles (double-buffered)
+  uint8_t *sH0 = sF + 2 * TILE;                // h_0 tile
   uint8_t *sW0 = sH0 + TILE;                   // W_0 / 2
   uint8_t *sOnesK = sW0 + (size_t)H * H * 2;
   uint8_t *sBias = sOnesK + LY::ONES_K;
@@ -61,16 +61,15 @@ __global__ void __launch_bounds__(Dw01Layout<H>::NT, 1) k_dw01(Dw01Params p) {
   float4 *sB4 = reinterpret_cast<float4 *>(sOnesN + LY::ONES_N);
   uint64_t *bars = reinterpret_cast<uint64_t *>(sB4 + C);
   uint64_t *full = bars, *empty = bars + LY::NST;          // delta stages
-  // F / h_0 tiles and the y accumulator are single-buffered; the feature warps run one tile ahead:
-  //   f_full (8 warps)  F(t) written          -> y(t) MMA, dW_0(t)
-  //   f_free (commit)   dW_0(t) read F(t)     -> F(t+1) may be written
+  //   fbar[b] (tx)      F(t) landed in slot b = t % 2
+  //   f_free[b] (commit) y(t) and dW_0(t) have read F slot b
   //   y_full (commit)   y(t) in TMEM          -> Swish(t)
-  //   y_free (8 warps)  Swish(t) loaded y(t)  -> y(t+1) MMA may overwrite it
-  //   h_full (8 warps)  h_0(t) written        -> dW_1(t)
+  //   y_free (NFW warps) Swish(t) loaded y(t) -> y(t+1) MMA may overwrite it
+  //   h_full (NFW warps) h_0(t) written       -> dW_1(t)
   //   h_free (commit)   dW_1(t) read h_0(t)   -> h_0(t+1) may be written
-  uint64_t *f_full = bars + 2 * LY::NST, *f_free = f_full + 1, *y_full = f_full + 2, *y_free = f_full + 3;
-  uint64_t *h_full = f_full + 4, *h_free = f_full + 5, *w_bar = f_full + 6, *done = f_full + 7;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(f_full + 8);
+  uint64_t *fbar = bars + 2 * LY::NST, *f_free = fbar + 2, *y_full = fbar + 4, *y_free = fbar + 5;
+  uint64_t *h_full = fbar + 6, *h_free = fbar + 7, *w_bar = fbar + 8, *done = fbar + 9;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(fbar + 10);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (warp == 0) {
@@ -82,8 +81,10 @@ __global__ void __launch_bounds__(Dw01Layout<H>::NT, 1) k_dw01(Dw01Params p) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(f_full, LY::NFW);
-    mbar_init(f_free, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&fbar[b], 1);
+      mbar_init(&f_free[b], 1);
+    }
     mbar_init(y_full, 1);
     mbar_init(y_free, LY::NFW);
     mbar_init(h_full, LY::NFW);
@@ -94,7 +95,6 @@ __global__ void __launch_bounds__(Dw01Layout<H>::NT, 1) k_dw01(Dw01Params p) {
   }
   for (int i = tid; i < (int)(LY::ONES_K + LY::BIAS_B) / 4; i += LY::NT) reinterpret_cast<uint32_t *>(sOnesK)[i] = 0u;
   for (int i = tid; i < (int)LY::ONES_N / 4; i += LY::NT) reinterpret_cast<uint32_t *>(sOnesN)[i] = 0x3F803F80u;
-  for (int i = tid; i < C; i += LY::NT) sB4[i] = reinterpret_cast<const float4 *>(p.B)[i];
   __syncthreads();
   for (int i = tid; i < 128; i += LY::NT) {
     *reinterpret_cast<__nv_bfloat16 *>(sOnesK + nosw16_offset(i, 0)) = __float2bfloat16_rn(1.f);
@@ -118,25 +118,21 @@ __global__ void __launch_bounds__(Dw01Layout<H>::NT, 1) k_dw01(Dw01Params p) {
   for (int64_t t = split; t < p.n_tiles; t += ks) ++count;
 
   if (warp == 0) {
-    if (lane == 0) {  // ------------------------------------------- delta loads (+ W_0 once)
+    if (lane == 0) {  // ------------------------------------------- F / delta loads (+ W_0 once)
       mbar_arrive_expect_tx(w_bar, H * H * 2);
       bulk_g2s(sW0, p.wpack_half, H * H * 2, w_bar);
-      constexpr int kAhead = 4;  // tiles prefetched into L2 beyond the 3-slot smem ring
-      for (int a = 1; a <= kAhead; ++a) {
-        const int64_t t = split + (int64_t)a * ks;
-        if (t < p.n_tiles)
-          for (int l = 0; l < 2; ++l) bulk_prefetch_l2(p.dstash + ((size_t)l * p.n_tiles + t) * TILE, TILE);
-      }
-      int k = 0;
-      for (int64_t t = split; t < p.n_tiles; t += ks)
-        for (int l = 0; l < 2; ++l, ++k) {
-          const int64_t tp = t + (int64_t)(kAhead + 1) * ks;
-          if (tp < p.n_tiles) bulk_prefetch_l2(p.dstash + ((size_t)l * p.n_tiles + tp) * TILE, TILE);
-          const int st = k % LY::NST;
-          if (k >= LY::NST) mbar_wait_sleep(&empty[st], ((k / LY::NST) - 1) & 1, 1000);
-          mbar_arrive_expect_tx(&full[st], TILE);
-          bulk_g2s(sD + st * TILE, p.dstash + ((size_t)l * p.n_tiles + t) * TILE, TILE, &full[st]);
+      int it = 0;
+      for (int64_t t = split; t < p.n_tiles; t += ks, ++it) {
+        const int fb = it & 1;
+        if (it >= 2) mbar_wait_sleep(&f_free[fb], ((it - 2) >> 1) & 1, 1000);
+        mbar_arrive_expect_tx(&fbar[fb], TILE);
+        bulk_g2s(sF + fb * TILE, p.fstash + (size_t)t * TILE, TILE, &fbar[fb]);
+        for (int l = 0; l < 2; ++l) {
+          if (it >= 1) mbar_wait_sleep(&empty[l], (it - 1) & 1, 1000);
+          mbar_arrive_expect_tx(&full[l], TILE);
+          bulk_g2s(sD + l * TILE, p.dstash + ((size_t)l * p.n_tiles + t) * TILE, TILE, &full[l]);
         }
+      }
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ------------------------------------------- MMA issuer
@@ -144,35 +140,34 @@ __global__ void __launch_bounds__(Dw01Layout<H>::NT, 1) k_dw01(Dw01Params p) {
       const uint32_t f_base = smem_u32(sF), h_base = smem_u32(sH0), w0 = smem_u32(sW0), on = smem_u32(sOnesN);
       mbar_wait(w_bar, 0);
       auto y_mma = [&](int it) {  // y(t) = gamma(x) W_0^T / 2 + b_0 / 2 into t_y
-        mbar_wait(f_full, it & 1);
+        const uint32_t fbase = f_base + (it & 1) * TILE;
+        mbar_wait(&fbar[it & 1], (it >> 1) & 1);
         if (it > 0) mbar_wait(y_free, (it - 1) & 1);  // Swish(t-1) has loaded its y
         tc_fence_after();
         umma_bf16(t_y, sdesc_none(smem_u32(sOnesK), 128, 256), sdesc_none(smem_u32(sBias), 128, 256), idf, 0u);
 #pragma unroll
         for (int kk = 0; kk < H / 16; ++kk)
-          umma_bf16(t_y, sdesc_sw128(f_base + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
+          umma_bf16(t_y, sdesc_sw128(fbase + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
                     sdesc_sw128(w0 + (kk >> 2) * (H * 128) + (kk & 3) * 32, 16, 1024), idf, 1u);
         umma_commit(y_full);
       };
       if (count > 0) y_mma(0);
       for (int it = 0; it < count; ++it) {
-        const int k0 = 2 * it, k1 = 2 * it + 1;
-        const int st0 = k0 % LY::NST, st1 = k1 % LY::NST;
-        const uint32_t d0 = smem_u32(sD + st0 * TILE), d1 = smem_u32(sD + st1 * TILE);
-        mbar_wait(&full[st0], (k0 / LY::NST) & 1);  // delta_0 of this tile
+        const uint32_t d0 = smem_u32(sD), d1 = d0 + TILE, fbase = f_base + (it & 1) * TILE;
+        mbar_wait(&full[0], it & 1);  // delta_0 of this tile
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {  // layer 0: operand gamma(x)
           const uint32_t acc = (it > 0 || kk > 0) ? 1u : 0u;
-          umma_bf16(t_dw0, sdesc_sw128(d0 + kk * 2048, 16384, 1024), sdesc_sw128(f_base + kk * 2048, 16384, 1024), idw,
+          umma_bf16(t_dw0, sdesc_sw128(d0 + kk * 2048, 16384, 1024), sdesc_sw128(fbase + kk * 2048, 16384, 1024), idw,
                     acc);
           umma_bf16(t_db0, sdesc_sw128(d0 + kk * 2048, 16384, 1024), sdesc_sw128(on + (kk & 3) * 32, 16, 1024), idb, acc);
         }
-        umma_commit(&empty[st0]);
-        umma_commit(f_free);
-        if (it + 1 < count) y_mma(it + 1);  // overlaps Swish(t) on the feature warps
-        mbar_wait(&full[st1], (k1 / LY::NST) & 1);  // delta_1
-        mbar_wait(h_full, it & 1);                 // h_0 of this tile in sH0
+        umma_commit(&empty[0]);
+        umma_commit(&f_free[it & 1]);
+        if (it + 1 < count) y_mma(it + 1);  // overlaps Swish(t) on the epilogue warps
+        mbar_wait(&full[1], it & 1);  // delta_1
+        mbar_wait(h_full, it & 1);    // h_0 of this tile in sH0
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
@@ -181,7 +176,7 @@ __global__ void __launch_bounds__(Dw01Layout<H>::NT, 1) k_dw01(Dw01Params p) {
                     acc);
           umma_bf16(t_db1, sdesc_sw128(d1 + kk * 2048, 16384, 1024), sdesc_sw128(on + (kk & 3) * 32, 16, 1024), idb, acc);
         }
-        umma_commit(&empty[st1]);
+        umma_commit(&empty[1]);
         umma_commit(h_free);
       }
       umma_commit(done);
@@ -192,33 +187,8 @@ __global__ void __launch_bounds__(Dw01Layout<H>::NT, 1) k_dw01(Dw01Params p) {
     const int row = ((warp & 3) << 5) | lane, half = (warp - 2) >> 2;  // half = column part 0..NQ-1
     const uint32_t f_base = smem_u32(sF), h_base = smem_u32(sH0);
     const uint32_t trow = t_y + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(half * (H / NQ));
-    constexpr int NFC = (C / NQ) / 8;
-    auto features = [&](int64_t t, int it, const RayRec &rr) {  // gamma(x) of tile t -> F
-      const int64_t g = t * 128 + row;
-      const float4 rb = grff_coords_from(rr, g, p.lg_ns, p.n_s, g < p.nsamp, p.jit);
-      uint32_t pc[NFC][4], ps[NFC][4];
-#pragma unroll
-      for (int fc = 0; fc < NFC; ++fc) grff8(sB4, half * (C / NQ) + 8 * fc, rb, pc[fc], ps[fc]);
-      if (it > 0) mbar_wait_sleep(f_free, (it - 1) & 1, 1000);
-#pragma unroll
-      for (int fc = 0; fc < NFC; ++fc) {
-        const int c0 = half * (C / NQ) + 8 * fc;
-        st_shared_v4(f_base + sw128_offset(row, c0, 128), pc[fc][0], pc[fc][1], pc[fc][2], pc[fc][3]);
-        st_shared_v4(f_base + sw128_offset(row, C + c0, 128), ps[fc][0], ps[fc][1], ps[fc][2], ps[fc][3]);
-      }
-      fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(f_full);
-    };
-    if (count > 0) {
-      const int64_t g = (int64_t)split * 128 + row;
-      features(split, 0, grff_fetch(p.rec32, g, p.lg_ns, g < p.nsamp));
-    }
     int it = 0;
     for (int64_t t = split; t < p.n_tiles; t += ks, ++it) {
-      // ray records of the next tile: in flight while this tile's y is read
-      const int64_t gn = (t + ks) * 128 + row;
-      const RayRec rn = grff_fetch(p.rec32, gn, p.lg_ns, t + ks < p.n_tiles && gn < p.nsamp);
       // h_0 = swish(y_0) of tile t: y = z / 2 from the prescaled MMA, h = y (1 + tanh y)
       mbar_wait_sleep(y_full, it & 1, 1000);
       tc_fence_after();
@@ -235,8 +205,6 @@ __global__ void __launch_bounds__(Dw01Layout<H>::NT, 1) k_dw01(Dw01Params p) {
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(y_free);  // y(t+1) may now be computed into TMEM
-      // the next tile's features overlap the y(t+1) MMA's wait for them and this tile's Swish
-      if (t + ks < p.n_tiles) features(t + ks, it + 1, rn);
 #pragma unroll
       for (int hc = 0; hc < NHC; ++hc)
 #pragma unroll
