@@ -334,12 +334,12 @@ dinr_status launch_tc_mlp(dinr_ctx *c, const Plan &pl, bool train, cudaStream_t 
     dinr_status s = set_smem(c, k_tc_mlp<H, true>, smem);
     if (s) return s;
     Launch L_(c, T_BWD, st);
-    k_tc_mlp<H, true><<<pl.grid_tc, 128, smem, st>>>(p);
+    k_tc_mlp<H, true><<<pl.grid_tc, kTcThreads, smem, st>>>(p);
   } else {
     dinr_status s = set_smem(c, k_tc_mlp<H, false>, smem);
     if (s) return s;
     Launch L_(c, T_FWD, st);
-    k_tc_mlp<H, false><<<pl.grid_tc, 128, smem, st>>>(p);
+    k_tc_mlp<H, false><<<pl.grid_tc, kTcThreads, smem, st>>>(p);
   }
   CUDA_TRY(c, cudaGetLastError());
   return DINR_OK;
@@ -1149,7 +1149,7 @@ dinr_status launch_infer(dinr_ctx *c, const VoxGrid &vg, int64_t n_vox, float *o
   const int64_t tiles = (n_vox + 127) / 128;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)c->sm_count * tc_occupancy(c)));
   Launch L_(c, T_FWD, st);
-  k_tc_mlp<H, false><<<grid, 128, smem, st>>>(p);
+  k_tc_mlp<H, false><<<grid, kTcThreads, smem, st>>>(p);
   CUDA_TRY(c, cudaGetLastError());
   return DINR_OK;
 }

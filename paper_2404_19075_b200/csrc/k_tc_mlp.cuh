@@ -49,7 +49,7 @@ struct TcLayout {
   static constexpr uint32_t W_LAYER = H * H * 2u;
   static size_t smem_bytes(int L, bool resident) {
     size_t w = resident ? (size_t)L * W_LAYER : W_LAYER;
-    return 1024 + A_BYTES + w + (size_t)L * H * 4 + H * 4 + 16 + (H / 2) * 16 + 64;
+    return 1024 + A_BYTES + w + (size_t)L * H * 4 + H * 4 + 16 + (H / 2) * 16 + 64 + 2 * 128 * 4;
   }
 };
 
@@ -59,8 +59,12 @@ __device__ __forceinline__ float dswish_f(float z) {
   return s * (1.f + z * (1.f - s));
 }
 
+// 256 threads: thread = (TMEM lane / sample row, column half cg); every MMA is issued as two
+// N = H/2 halves with their own commit, so half cg's epilogue starts while the other half computes.
+constexpr int kTcThreads = 256;
+
 template <int H, bool TRAIN>
-__global__ void __launch_bounds__(128, 1) k_tc_mlp(TcParams p) {
+__global__ void __launch_bounds__(kTcThreads, 1) k_tc_mlp(TcParams p) {
   constexpr int C = H / 2;
   constexpr uint32_t A_BYTES = TcLayout<H>::A_BYTES;
   constexpr uint32_t W_LAYER = TcLayout<H>::W_LAYER;
@@ -74,8 +78,8 @@ __global__ void __launch_bounds__(128, 1) k_tc_mlp(TcParams p) {
   float *sWo = sBias + L * H;
   float *sB = sWo + H + 4;
   uint64_t *bars = reinterpret_cast<uint64_t *>(sB + C * 4);
-  uint64_t *mma_bar = bars, *w_bar = bars + 1;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2);
+  uint64_t *mma_bar = bars, *w_bar = bars + 2;  // mma_bar[cg]: N-half cg of the current MMA retired
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 3);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (warp == 0) {
@@ -83,20 +87,24 @@ __global__ void __launch_bounds__(128, 1) k_tc_mlp(TcParams p) {
     tmem_relinquish();
   }
   if (tid == 0) {
-    mbar_init(mma_bar, 1);
+    mbar_init(&mma_bar[0], 1);
+    mbar_init(&mma_bar[1], 1);
     mbar_init(w_bar, 1);
     fence_mbar_init();
   }
   const int64_t per = (int64_t)H * H + H;
-  for (int i = tid; i < L * H; i += 128) sBias[i] = p.params[(i / H) * per + (int64_t)H * H + (i % H)];
-  for (int i = tid; i <= H; i += 128) sWo[i] = p.params[(int64_t)L * per + i];  // w_o, then b_o
-  for (int i = tid; i < C * 4; i += 128) sB[i] = p.B[i];
+  for (int i = tid; i < L * H; i += kTcThreads) sBias[i] = p.params[(i / H) * per + (int64_t)H * H + (i % H)];
+  for (int i = tid; i <= H; i += kTcThreads) sWo[i] = p.params[(int64_t)L * per + i];  // w_o, then b_o
+  for (int i = tid; i < C * 4; i += kTcThreads) sB[i] = p.B[i];
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t a_base = smem_u32(sA), w_base = smem_u32(sW);
-  const uint32_t tmem_row = tmem + ((uint32_t)(warp * 32) << 16);
+  const uint32_t tmem_row = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+  const int cg = tid >> 7;                     // column half of this thread
+  const int cb_lo = cg * (H / 64), cb_hi = (cg + 1) * (H / 64);  // its 32-column chunks
+  float *sMu = reinterpret_cast<float *>(bars + 4);  // [2][128] per-half head partials (forward)
   const int n_tiles = (int)((p.nsamp + 127) / 128);
 
   // Weight schedule (thread 0): the layer whose image sits in sW, and a pending load.
@@ -127,12 +135,14 @@ __global__ void __launch_bounds__(128, 1) k_tc_mlp(TcParams p) {
 #pragma unroll
   for (int i = 0; i < H / 32; ++i) head_acc[i] = 0.f;
   float bo_acc = 0.f;
-  const uint32_t idesc_f = idesc_bf16(128, H, 0, 0);
-  const uint32_t idesc_b = idesc_bf16(128, H, 0, 1);
+  constexpr bool kSplit = H >= 128;  // N halves need whole 64-column blocks for the MN-major dX operand
+  constexpr int NH = kSplit ? H / 2 : H;
+  const uint32_t idesc_f = idesc_bf16(128, NH, 0, 0);
+  const uint32_t idesc_b = idesc_bf16(128, NH, 0, 1);
 
   for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
     const bool more_tiles = tile + (int)gridDim.x < n_tiles;
-    const int row = tid;
+    const int row = tid & 127;
     const int64_t g = (int64_t)tile * 128 + row;
     const bool valid = g < p.nsamp;
     bool inside = false;
@@ -162,7 +172,7 @@ __global__ void __launch_bounds__(128, 1) k_tc_mlp(TcParams p) {
         if (TRAIN) u_row = p.u[ray];
       }
 #pragma unroll 1
-      for (int c0 = 0; c0 < C; c0 += 8) {
+      for (int c0 = cg * (C / 2); c0 < (cg + 1) * (C / 2); c0 += 8) {
         uint32_t pc[4], ps[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -194,18 +204,23 @@ __global__ void __launch_bounds__(128, 1) k_tc_mlp(TcParams p) {
       if (tid == 0) {
         uint32_t wl = w_ready(l);
         tc_fence_after();
+        for (int half = 0; half < 2; ++half) {  // output columns [half NH, (half+1) NH)
+          if (half == 0 || kSplit) {
 #pragma unroll 4
-        for (int kk = 0; kk < H / 16; ++kk) {
-          uint64_t ad = sdesc_sw128(a_base + (kk >> 2) * (128 * 128) + (kk & 3) * 32, 16, 1024);
-          uint64_t bd = sdesc_sw128(wl + (kk >> 2) * (H * 128) + (kk & 3) * 32, 16, 1024);
-          umma_bf16(tmem, ad, bd, idesc_f, kk > 0 ? 1u : 0u);
+            for (int kk = 0; kk < H / 16; ++kk) {
+              uint64_t ad = sdesc_sw128(a_base + (kk >> 2) * (128 * 128) + (kk & 3) * 32, 16, 1024);
+              uint64_t bd = sdesc_sw128(wl + (kk >> 2) * (H * 128) + half * NH * 128 + (kk & 3) * 32, 16, 1024);
+              umma_bf16(tmem + half * NH, ad, bd, idesc_f, kk > 0 ? 1u : 0u);
+            }
+          }
+          umma_commit(&mma_bar[half]);
         }
-        umma_commit(mma_bar);
       }
-      mbar_wait(mma_bar, mma_phase);
+      mbar_wait(&mma_bar[cg], mma_phase);
       mma_phase ^= 1;
       tc_fence_after();
       if (tid == 0) {
+        mbar_wait(&mma_bar[1], mma_phase ^ 1);  // both halves retired before sW may be refilled
         // prefetch the next weight image (streaming mode) now that sW is free
         if (!resident) {
           int nxt;
@@ -224,7 +239,7 @@ __global__ void __launch_bounds__(128, 1) k_tc_mlp(TcParams p) {
       if (TRAIN) __syncthreads();
       const bool last = (l == L - 1);
 #pragma unroll 1
-      for (int cb = 0; cb < H / 32; ++cb) {
+      for (int cb = cb_lo; cb < cb_hi; ++cb) {
         uint32_t v[32];
         tmem_ld32(tmem_row + cb * 32, v);
         tmem_wait_ld();
@@ -294,37 +309,49 @@ __global__ void __launch_bounds__(128, 1) k_tc_mlp(TcParams p) {
       }
     }
     if (!TRAIN) {
-      // a9 ray-chunk sum of M = mu0 (w_o . h_L + b_o) over the warp's 32 samples
-      float mu = p.mu0 * (mu_acc + sWo[H]);
-      if (p.grid_mode) {
-        if (valid) p.vout[g] = inside ? mu : 0.f;
-      } else {
+      // a9 ray-chunk sum of M = mu0 (w_o . h_L + b_o) over the warp's 32 samples (the two column
+      // halves of a row meet in shared memory)
+      sMu[cg * 128 + row] = mu_acc;
+      __syncthreads();
+      if (cg == 0) {
+        float mu = p.mu0 * (sMu[row] + sMu[128 + row] + sWo[H]);
+        if (p.grid_mode) {
+          if (valid) p.vout[g] = inside ? mu : 0.f;
+        } else {
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) mu += __shfl_xor_sync(0xffffffffu, mu, o);
-        if (lane == 0 && valid) p.pchunk[g >> 5] = mu;
+          for (int o = 16; o > 0; o >>= 1) mu += __shfl_xor_sync(0xffffffffu, mu, o);
+          if (lane == 0 && valid) p.pchunk[g >> 5] = mu;
+        }
       }
     } else {
-      float us = u_row;
+      if (cg == 0) {
+        float us = u_row;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) us += __shfl_xor_sync(0xffffffffu, us, o);
-      bo_acc += us;
+        for (int o = 16; o > 0; o >>= 1) us += __shfl_xor_sync(0xffffffffu, us, o);
+        bo_acc += us;
+      }
       // ------------------------------------------------------------ a12 backward dX chain
       for (int l = L - 1; l >= 1; --l) {
         if (tid == 0) {
           uint32_t wl = w_ready(l);
           tc_fence_after();
+          for (int half = 0; half < 2; ++half) {  // input columns [half NH, (half+1) NH)
+            if (half == 0 || kSplit) {
 #pragma unroll 4
-          for (int kk = 0; kk < H / 16; ++kk) {
-            uint64_t ad = sdesc_sw128(a_base + (kk >> 2) * (128 * 128) + (kk & 3) * 32, 16, 1024);
-            uint64_t bd = sdesc_sw128(wl + kk * 2048, H * 128, 1024);  // MN-major W_l
-            umma_bf16(tmem, ad, bd, idesc_b, kk > 0 ? 1u : 0u);
+              for (int kk = 0; kk < H / 16; ++kk) {
+                uint64_t ad = sdesc_sw128(a_base + (kk >> 2) * (128 * 128) + (kk & 3) * 32, 16, 1024);
+                uint64_t bd = sdesc_sw128(wl + half * (NH / 64) * (H * 128) + kk * 2048, H * 128, 1024);  // MN-major W_l
+                umma_bf16(tmem + half * NH, ad, bd, idesc_b, kk > 0 ? 1u : 0u);
+              }
+            }
+            umma_commit(&mma_bar[half]);
           }
-          umma_commit(mma_bar);
         }
-        mbar_wait(mma_bar, mma_phase);
+        mbar_wait(&mma_bar[cg], mma_phase);
         mma_phase ^= 1;
         tc_fence_after();
         if (tid == 0) {
+          mbar_wait(&mma_bar[1], mma_phase ^ 1);
           if (!resident) {
             int nxt = (l - 1 >= 1) ? l - 1 : 0;
             bool has_next = (l - 1 >= 1) || more_tiles;
@@ -335,7 +362,7 @@ __global__ void __launch_bounds__(128, 1) k_tc_mlp(TcParams p) {
         __syncthreads();
         const uint4 *zsrc = reinterpret_cast<const uint4 *>(p.zstash) + (((size_t)(l - 1) * p.n_tiles + tile) * (H / 8)) * 128 + row;
 #pragma unroll 1
-        for (int cb = 0; cb < H / 32; ++cb) {
+        for (int cb = cb_lo; cb < cb_hi; ++cb) {
           uint32_t v[32];
           tmem_ld32(tmem_row + cb * 32, v);
           uint4 zq[4];
@@ -373,12 +400,14 @@ __global__ void __launch_bounds__(128, 1) k_tc_mlp(TcParams p) {
     if (tid == 0) bulk_wait_read_all();
     __syncthreads();
 #pragma unroll
-    for (int cb = 0; cb < H / 32; ++cb) red[warp * (H + 1) + cb * 32 + lane] = head_acc[cb];
-    if (lane == 0) red[warp * (H + 1) + H] = bo_acc;
+    for (int cb = 0; cb < H / 32; ++cb)
+      if (cb >= cb_lo && cb < cb_hi) red[warp * (H + 1) + cb * 32 + lane] = head_acc[cb];
+    if (lane == 0) red[warp * (H + 1) + H] = bo_acc;  // (zero for column-half-1 warps)
     __syncthreads();
-    for (int k = tid; k <= H; k += 128) {
+    for (int k = tid; k <= H; k += kTcThreads) {
       float acc = 0.f;
-      for (int w = 0; w < 4; ++w) acc += red[w * (H + 1) + k];
+      const int w0 = (k < H && k >= H / 2) ? 4 : 0;  // the 4 warps of the column half holding k
+      for (int w = w0; w < w0 + 4; ++w) acc += red[w * (H + 1) + k];
       p.head_part[(size_t)blockIdx.x * (H + 1) + k] = acc;
     }
     if (tid == 0) bulk_wait_all();
