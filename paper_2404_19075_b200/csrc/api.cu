@@ -217,7 +217,7 @@ size_t plan_layout(dinr_ctx *c, int64_t n, bool train, bool host_io, Plan &pl, v
   } else if (!simt && train) {
     pl.hstash = ar.take<uint8_t>((size_t)L * pl.n_tiles * H * 256);
     pl.dstash = ar.take<uint8_t>((size_t)L * pl.n_tiles * H * 256);
-    pl.zstash = ar.take<uint8_t>((size_t)std::max(1, L - 1) * pl.n_tiles * H * 256);
+    pl.zstash = ar.take<uint8_t>((size_t)L * pl.n_tiles * H * 256);
   }
   if (simt) {
     pl.sh = ar.take<float>((size_t)(L + 1) * pl.nsamp * H);
@@ -310,7 +310,7 @@ FieldDev field_dev(const dinr_ctx *c) {
 }
 
 template <int H>
-dinr_status launch_tc_mlp(dinr_ctx *c, const Plan &pl, bool train, cudaStream_t st) {
+dinr_status launch_tc_mlp(dinr_ctx *c, const Plan &pl, int mode, cudaStream_t st) {
   TcParams p{};
   p.jit = pl.jit;
   p.rec32 = pl.rec32;
@@ -330,16 +330,21 @@ dinr_status launch_tc_mlp(dinr_ctx *c, const Plan &pl, bool train, cudaStream_t 
   p.head_part = pl.head_part;
   p.n_tiles = pl.n_tiles;
   size_t smem = TcLayout<H>::smem_bytes(c->L, p.resident != 0);
-  if (train) {
-    dinr_status s = set_smem(c, k_tc_mlp<H, true>, smem);
+  if (mode == 2) {
+    dinr_status s = set_smem(c, k_tc_mlp<H, 2>, smem);
     if (s) return s;
     Launch L_(c, T_BWD, st);
-    k_tc_mlp<H, true><<<pl.grid_tc, kTcThreads, smem, st>>>(p);
-  } else {
-    dinr_status s = set_smem(c, k_tc_mlp<H, false>, smem);
+    k_tc_mlp<H, 2><<<pl.grid_tc, kTcThreads, smem, st>>>(p);
+  } else if (mode == 1) {
+    dinr_status s = set_smem(c, k_tc_mlp<H, 1>, smem);
     if (s) return s;
     Launch L_(c, T_FWD, st);
-    k_tc_mlp<H, false><<<pl.grid_tc, kTcThreads, smem, st>>>(p);
+    k_tc_mlp<H, 1><<<pl.grid_tc, kTcThreads, smem, st>>>(p);
+  } else {
+    dinr_status s = set_smem(c, k_tc_mlp<H, 0>, smem);
+    if (s) return s;
+    Launch L_(c, T_FWD, st);
+    k_tc_mlp<H, 0><<<pl.grid_tc, kTcThreads, smem, st>>>(p);
   }
   CUDA_TRY(c, cudaGetLastError());
   return DINR_OK;
@@ -454,11 +459,11 @@ dinr_status launch_fused(dinr_ctx *c, const Plan &pl, const float *y, cudaStream
   return DINR_OK;
 }
 
-dinr_status tc_forward(dinr_ctx *c, const Plan &pl, bool train, cudaStream_t st) {
+dinr_status tc_forward(dinr_ctx *c, const Plan &pl, int mode, cudaStream_t st) {
   switch (c->H) {
-    case 64: return launch_tc_mlp<64>(c, pl, train, st);
-    case 128: return launch_tc_mlp<128>(c, pl, train, st);
-    case 256: return launch_tc_mlp<256>(c, pl, train, st);
+    case 64: return launch_tc_mlp<64>(c, pl, mode, st);
+    case 128: return launch_tc_mlp<128>(c, pl, mode, st);
+    case 256: return launch_tc_mlp<256>(c, pl, mode, st);
   }
   return fail(c, DINR_EINVAL, "unsupported width");
 }
@@ -660,7 +665,7 @@ dinr_status step_grad(dinr_ctx *c, const int64_t *idx, int64_t n, const float *y
   if (simt) {
     s = simt_forward(c, pl, st);
   } else {
-    s = tc_forward(c, pl, false, st);
+    s = tc_forward(c, pl, 1, st);  // training forward: stashes h_l and z_l for K3 / K5
   }
   if (s) return s;
   s = run_loss(c, pl, y, pl.fhat, nullptr, nullptr, nullptr, st);
@@ -671,7 +676,7 @@ dinr_status step_grad(dinr_ctx *c, const int64_t *idx, int64_t n, const float *y
     nhead = pl.ksplit_simt;
     ks = pl.ksplit_simt;
   } else {
-    s = tc_forward(c, pl, true, st);
+    s = tc_forward(c, pl, 2, st);  // backward from the stashes
     if (s) return s;
     s = tc_dw(c, pl, st);
     nhead = pl.grid_tc;
@@ -944,7 +949,7 @@ dinr_status dinr_project(dinr_ctx *c, const int64_t *idx, int64_t n, float *fhat
   if (s) return s;
   s = launch_rays(c, idx, n, nullptr, pl.rec32, pl.jit.rid ? pl.rid : nullptr, st);
   if (s) return s;
-  s = c->field.precision == DINR_FP32_VERIFY ? simt_forward(c, pl, st) : tc_forward(c, pl, false, st);
+  s = c->field.precision == DINR_FP32_VERIFY ? simt_forward(c, pl, st) : tc_forward(c, pl, 0, st);
   if (s) return s;
   return run_loss(c, pl, nullptr, fhat, p_sub, I0, Ihat, st);
 }
@@ -1144,12 +1149,12 @@ dinr_status launch_infer(dinr_ctx *c, const VoxGrid &vg, int64_t n_vox, float *o
   p.vg = vg;
   p.vout = out;
   const size_t smem = TcLayout<H>::smem_bytes(c->L, p.resident != 0);
-  dinr_status s = set_smem(c, k_tc_mlp<H, false>, smem);
+  dinr_status s = set_smem(c, k_tc_mlp<H, 0>, smem);
   if (s) return s;
   const int64_t tiles = (n_vox + 127) / 128;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)c->sm_count * tc_occupancy(c)));
   Launch L_(c, T_FWD, st);
-  k_tc_mlp<H, false><<<grid, kTcThreads, smem, st>>>(p);
+  k_tc_mlp<H, 0><<<grid, kTcThreads, smem, st>>>(p);
   CUDA_TRY(c, cudaGetLastError());
   return DINR_OK;
 }

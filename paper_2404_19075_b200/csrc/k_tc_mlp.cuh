@@ -63,8 +63,13 @@ __device__ __forceinline__ float dswish_f(float z) {
 // N = H/2 halves with their own commit, so half cg's epilogue starts while the other half computes.
 constexpr int kTcThreads = 256;
 
-template <int H, bool TRAIN>
+// MODE 0: forward (projection / voxels: ray-chunk sums or per-voxel values)
+// MODE 1: training forward: as 0, plus bulk stores of every layer input h_l and fp16 z_l stores
+// MODE 2: training backward from the stashes: top-layer delta and head gradients from z_{L-1},
+//         then the dX chain (K3); no forward recompute
+template <int H, int MODE>
 __global__ void __launch_bounds__(kTcThreads, 1) k_tc_mlp(TcParams p) {
+  constexpr bool TRAIN = MODE == 2;
   constexpr int C = H / 2;
   constexpr uint32_t A_BYTES = TcLayout<H>::A_BYTES;
   constexpr uint32_t W_LAYER = TcLayout<H>::W_LAYER;
@@ -128,7 +133,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_mlp(TcParams p) {
     }
     return resident ? w_base + (uint32_t)layer * W_LAYER : w_base;
   };
-  if (tid == 0 && (int)blockIdx.x < n_tiles) w_issue(0);
+  if (tid == 0 && (int)blockIdx.x < n_tiles && (MODE != 2 || L >= 2)) w_issue(MODE == 2 ? L - 1 : 0);
 
   uint32_t mma_phase = 0;
   float head_acc[H / 32];
@@ -146,114 +151,101 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_mlp(TcParams p) {
     const int64_t g = (int64_t)tile * 128 + row;
     const bool valid = g < p.nsamp;
     bool inside = false;
-    float u_row = 0.f;
-    if (TRAIN) {  // the previous tile's last bulk store must be done reading sA
+    if (MODE != 0) {  // the previous tile's last bulk store must be done reading sA
       if (tid == 0) bulk_wait_read_all();
       __syncthreads();
     }
-    // ---------------------------------------------------------------- a5/a6 features
-    {
-      float rb0 = 0.f, rb1 = 0.f, rb2 = 0.f, rb3 = 0.f;
-      if (!TRAIN && p.grid_mode) {
-        const float4 r = voxel_coords(p.vg, valid ? g : 0, inside);
-        rb0 = r.x;
-        rb1 = r.y;
-        rb2 = r.z;
-        rb3 = r.w;
-      } else if (valid) {
-        int64_t ray = g / p.n_s;
-        const uint32_t jr = (uint32_t)(g - ray * p.n_s);
-        float jj = (float)jr + sample_offset(p.jit, ray, jr);
-        float4 ra = p.rec32[2 * ray], rbv = p.rec32[2 * ray + 1];
-        rb0 = ra.w;                 // t
-        rb1 = ra.z + jj * rbv.z;    // z
-        rb2 = ra.y + jj * rbv.y;    // y
-        rb3 = ra.x + jj * rbv.x;    // x
-        if (TRAIN) u_row = p.u[ray];
-      }
+    if (MODE != 2) {
+      // ---------------------------------------------------------------- a5/a6 features
+      {
+        float rb0 = 0.f, rb1 = 0.f, rb2 = 0.f, rb3 = 0.f;
+        if (MODE == 0 && p.grid_mode) {
+          const float4 r = voxel_coords(p.vg, valid ? g : 0, inside);
+          rb0 = r.x;
+          rb1 = r.y;
+          rb2 = r.z;
+          rb3 = r.w;
+        } else if (valid) {
+          int64_t ray = g / p.n_s;
+          const uint32_t jr = (uint32_t)(g - ray * p.n_s);
+          float jj = (float)jr + sample_offset(p.jit, ray, jr);
+          float4 ra = p.rec32[2 * ray], rbv = p.rec32[2 * ray + 1];
+          rb0 = ra.w;                 // t
+          rb1 = ra.z + jj * rbv.z;    // z
+          rb2 = ra.y + jj * rbv.y;    // y
+          rb3 = ra.x + jj * rbv.x;    // x
+        }
 #pragma unroll 1
-      for (int c0 = cg * (C / 2); c0 < (cg + 1) * (C / 2); c0 += 8) {
-        uint32_t pc[4], ps[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          float cs[2], sn[2];
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const float *bb = sB + 4 * (c0 + 2 * q + e);
-            float phi = bb[0] * rb0 + bb[1] * rb1 + bb[2] * rb2 + bb[3] * rb3;
-            float fr = phi - rintf(phi);  // range reduction to [-1/2, 1/2]
-            __sincosf(6.283185307179586f * fr, &sn[e], &cs[e]);
-          }
-          pc[q] = pack_bf16x2(cs[0], cs[1]);
-          ps[q] = pack_bf16x2(sn[0], sn[1]);
-        }
-        st_shared_v4(a_base + sw128_offset(row, c0, 128), pc[0], pc[1], pc[2], pc[3]);
-        st_shared_v4(a_base + sw128_offset(row, C + c0, 128), ps[0], ps[1], ps[2], ps[3]);
-      }
-    }
-    fence_proxy_async_smem();
-    tc_fence_before();
-    __syncthreads();
-    if (TRAIN && tid == 0) {
-      bulk_s2g(p.hstash + ((size_t)0 * p.n_tiles + tile) * A_BYTES, sA, A_BYTES);
-      bulk_commit();
-    }
-    // ---------------------------------------------------------------- a7/a8 forward
-    float mu_acc = 0.f;
-    for (int l = 0; l < L; ++l) {
-      if (tid == 0) {
-        uint32_t wl = w_ready(l);
-        tc_fence_after();
-        for (int half = 0; half < 2; ++half) {  // output columns [half NH, (half+1) NH)
-          if (half == 0 || kSplit) {
-#pragma unroll 4
-            for (int kk = 0; kk < H / 16; ++kk) {
-              uint64_t ad = sdesc_sw128(a_base + (kk >> 2) * (128 * 128) + (kk & 3) * 32, 16, 1024);
-              uint64_t bd = sdesc_sw128(wl + (kk >> 2) * (H * 128) + half * NH * 128 + (kk & 3) * 32, 16, 1024);
-              umma_bf16(tmem + half * NH, ad, bd, idesc_f, kk > 0 ? 1u : 0u);
-            }
-          }
-          umma_commit(&mma_bar[half]);
-        }
-      }
-      mbar_wait(&mma_bar[cg], mma_phase);
-      mma_phase ^= 1;
-      tc_fence_after();
-      if (tid == 0) {
-        mbar_wait(&mma_bar[1], mma_phase ^ 1);  // both halves retired before sW may be refilled
-        // prefetch the next weight image (streaming mode) now that sW is free
-        if (!resident) {
-          int nxt;
-          bool has_next = true;
-          if (!TRAIN) {
-            nxt = (l + 1) % L;
-            has_next = (l + 1 < L) || more_tiles;
-          } else {
-            nxt = (l + 1 < L) ? l + 1 : (L >= 2 ? L - 1 : 0);
-            has_next = (l + 1 < L) || L >= 2 || more_tiles;
-          }
-          if (has_next && nxt != w_cur) w_issue(nxt);
-        }
-        if (TRAIN) bulk_wait_read_all();
-      }
-      if (TRAIN) __syncthreads();
-      const bool last = (l == L - 1);
-#pragma unroll 1
-      for (int cb = cb_lo; cb < cb_hi; ++cb) {
-        uint32_t v[32];
-        tmem_ld32(tmem_row + cb * 32, v);
-        tmem_wait_ld();
-        float z[32];
-#pragma unroll
-        for (int i = 0; i < 32; ++i) z[i] = __uint_as_float(v[i]) + sBias[l * H + cb * 32 + i];
-        if (!last) {
+        for (int c0 = cg * (C / 2); c0 < (cg + 1) * (C / 2); c0 += 8) {
+          uint32_t pc[4], ps[4];
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
-            uint32_t w4[4];
+            float cs[2], sn[2];
 #pragma unroll
-            for (int e = 0; e < 4; ++e) w4[e] = pack_bf16x2(swish_f(z[8 * q + 2 * e]), swish_f(z[8 * q + 2 * e + 1]));
-            st_shared_v4(a_base + sw128_offset(row, cb * 32 + 8 * q, 128), w4[0], w4[1], w4[2], w4[3]);
-            if (TRAIN) {
+            for (int e = 0; e < 2; ++e) {
+              const float *bb = sB + 4 * (c0 + 2 * q + e);
+              float phi = bb[0] * rb0 + bb[1] * rb1 + bb[2] * rb2 + bb[3] * rb3;
+              float fr = phi - rintf(phi);  // range reduction to [-1/2, 1/2]
+              __sincosf(6.283185307179586f * fr, &sn[e], &cs[e]);
+            }
+            pc[q] = pack_bf16x2(cs[0], cs[1]);
+            ps[q] = pack_bf16x2(sn[0], sn[1]);
+          }
+          st_shared_v4(a_base + sw128_offset(row, c0, 128), pc[0], pc[1], pc[2], pc[3]);
+          st_shared_v4(a_base + sw128_offset(row, C + c0, 128), ps[0], ps[1], ps[2], ps[3]);
+        }
+      }
+      fence_proxy_async_smem();
+      tc_fence_before();
+      __syncthreads();
+      if (MODE == 1 && tid == 0) {  // layer 0's input for the dW GEMM
+        bulk_s2g(p.hstash + ((size_t)0 * p.n_tiles + tile) * A_BYTES, sA, A_BYTES);
+        bulk_commit();
+      }
+      // ---------------------------------------------------------------- a7/a8 forward
+      float mu_acc = 0.f;
+      for (int l = 0; l < L; ++l) {
+        if (tid == 0) {
+          uint32_t wl = w_ready(l);
+          tc_fence_after();
+          for (int half = 0; half < 2; ++half) {  // output columns [half NH, (half+1) NH)
+            if (half == 0 || kSplit) {
+#pragma unroll 4
+              for (int kk = 0; kk < H / 16; ++kk) {
+                uint64_t ad = sdesc_sw128(a_base + (kk >> 2) * (128 * 128) + (kk & 3) * 32, 16, 1024);
+                uint64_t bd = sdesc_sw128(wl + (kk >> 2) * (H * 128) + half * NH * 128 + (kk & 3) * 32, 16, 1024);
+                umma_bf16(tmem + half * NH, ad, bd, idesc_f, kk > 0 ? 1u : 0u);
+              }
+            }
+            umma_commit(&mma_bar[half]);
+          }
+        }
+        mbar_wait(&mma_bar[cg], mma_phase);
+        mma_phase ^= 1;
+        tc_fence_after();
+        if (tid == 0) {
+          mbar_wait(&mma_bar[1], mma_phase ^ 1);  // both halves retired before sW may be refilled
+          // prefetch the next weight image (streaming mode) now that sW is free
+          if (!resident) {
+            const int nxt = (l + 1) % L;
+            const bool has_next = (l + 1 < L) || more_tiles;
+            if (has_next && nxt != w_cur) w_issue(nxt);
+          }
+          if (MODE == 1) bulk_wait_read_all();
+        }
+        if (MODE == 1) __syncthreads();
+        const bool last = (l == L - 1);
+#pragma unroll 1
+        for (int cb = cb_lo; cb < cb_hi; ++cb) {
+          uint32_t v[32];
+          tmem_ld32(tmem_row + cb * 32, v);
+          tmem_wait_ld();
+          float z[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) z[i] = __uint_as_float(v[i]) + sBias[l * H + cb * 32 + i];
+          if (MODE == 1) {  // z_l (fp16, chunk-major) for swish' in the backward
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
               uint32_t h4[4];
 #pragma unroll
               for (int e = 0; e < 4; ++e) {
@@ -265,11 +257,62 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_mlp(TcParams p) {
               *dst = make_uint4(h4[0], h4[1], h4[2], h4[3]);
             }
           }
-        } else if (!TRAIN) {
+          if (!last) {
 #pragma unroll
-          for (int i = 0; i < 32; ++i) mu_acc += sWo[cb * 32 + i] * swish_f(z[i]);
+            for (int q = 0; q < 4; ++q) {
+              uint32_t w4[4];
+#pragma unroll
+              for (int e = 0; e < 4; ++e) w4[e] = pack_bf16x2(swish_f(z[8 * q + 2 * e]), swish_f(z[8 * q + 2 * e + 1]));
+              st_shared_v4(a_base + sw128_offset(row, cb * 32 + 8 * q, 128), w4[0], w4[1], w4[2], w4[3]);
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) mu_acc += sWo[cb * 32 + i] * swish_f(z[i]);
+          }
+        }
+        if (!last) fence_proxy_async_smem();
+        tc_fence_before();
+        __syncthreads();
+        if (MODE == 1 && !last && tid == 0) {  // input of layer l+1 for the dW GEMM
+          bulk_s2g(p.hstash + ((size_t)(l + 1) * p.n_tiles + tile) * A_BYTES, sA, A_BYTES);
+          bulk_commit();
+        }
+      }
+      // a9 ray-chunk sum of M = mu0 (w_o . h_L + b_o) over the warp's 32 samples (the two column
+      // halves of a row meet in shared memory)
+      sMu[cg * 128 + row] = mu_acc;
+      __syncthreads();
+      if (cg == 0) {
+        float mu = p.mu0 * (sMu[row] + sMu[128 + row] + sWo[H]);
+        if (MODE == 0 && p.grid_mode) {
+          if (valid) p.vout[g] = inside ? mu : 0.f;
         } else {
-          // head gradients (transpose-reduce u*h_L over the warp's 32 rows) and delta_L
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) mu += __shfl_xor_sync(0xffffffffu, mu, o);
+          if (lane == 0 && valid) p.pchunk[g >> 5] = mu;
+        }
+      }
+    } else {
+      // ---------------------------------------------------------------- a12 backward (MODE 2)
+      // top layer from the stashed z_{L-1}: h_L = swish(z) for the head gradients (transpose-
+      // reduce u h_L over the warp's 32 rows), delta_L = u w_o swish'(z)
+      const float u_row = valid ? p.u[g / p.n_s] : 0.f;
+      {
+        const uint4 *zsrc = reinterpret_cast<const uint4 *>(p.zstash) + (((size_t)(L - 1) * p.n_tiles + tile) * (H / 8)) * 128 + row;
+#pragma unroll 1
+        for (int cb = cb_lo; cb < cb_hi; ++cb) {
+          float z[32];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const uint4 zq = zsrc[(size_t)(cb * 4 + q) * 128];
+            const uint32_t zz[4] = {zq.x, zq.y, zq.z, zq.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float2 zf = __half22float2(*reinterpret_cast<const __half2 *>(&zz[e]));
+              z[8 * q + 2 * e] = zf.x;
+              z[8 * q + 2 * e + 1] = zf.y;
+            }
+          }
           float x[32];
 #pragma unroll
           for (int i = 0; i < 32; ++i) x[i] = u_row * swish_f(z[i]);
@@ -297,40 +340,21 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_mlp(TcParams p) {
             st_shared_v4(a_base + sw128_offset(row, cb * 32 + 8 * q, 128), w4[0], w4[1], w4[2], w4[3]);
           }
         }
-      }
-      if (!last || TRAIN) fence_proxy_async_smem();
-      tc_fence_before();
-      __syncthreads();
-      if (TRAIN && tid == 0) {
-        uint8_t *dst = last ? p.dstash + ((size_t)(L - 1) * p.n_tiles + tile) * A_BYTES
-                            : p.hstash + ((size_t)(l + 1) * p.n_tiles + tile) * A_BYTES;
-        bulk_s2g(dst, sA, A_BYTES);
-        bulk_commit();
-      }
-    }
-    if (!TRAIN) {
-      // a9 ray-chunk sum of M = mu0 (w_o . h_L + b_o) over the warp's 32 samples (the two column
-      // halves of a row meet in shared memory)
-      sMu[cg * 128 + row] = mu_acc;
-      __syncthreads();
-      if (cg == 0) {
-        float mu = p.mu0 * (sMu[row] + sMu[128 + row] + sWo[H]);
-        if (p.grid_mode) {
-          if (valid) p.vout[g] = inside ? mu : 0.f;
-        } else {
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) mu += __shfl_xor_sync(0xffffffffu, mu, o);
-          if (lane == 0 && valid) p.pchunk[g >> 5] = mu;
+        fence_proxy_async_smem();
+        tc_fence_before();
+        __syncthreads();
+        if (tid == 0) {
+          bulk_s2g(p.dstash + ((size_t)(L - 1) * p.n_tiles + tile) * A_BYTES, sA, A_BYTES);
+          bulk_commit();
         }
       }
-    } else {
       if (cg == 0) {
         float us = u_row;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) us += __shfl_xor_sync(0xffffffffu, us, o);
         bo_acc += us;
       }
-      // ------------------------------------------------------------ a12 backward dX chain
+      // dX chain
       for (int l = L - 1; l >= 1; --l) {
         if (tid == 0) {
           uint32_t wl = w_ready(l);
@@ -352,9 +376,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_mlp(TcParams p) {
         tc_fence_after();
         if (tid == 0) {
           mbar_wait(&mma_bar[1], mma_phase ^ 1);
-          if (!resident) {
-            int nxt = (l - 1 >= 1) ? l - 1 : 0;
-            bool has_next = (l - 1 >= 1) || more_tiles;
+          if (!resident) {  // next: layer l-1, or the next tile's top layer
+            const int nxt = (l - 1 >= 1) ? l - 1 : L - 1;
+            const bool has_next = (l - 1 >= 1) || more_tiles;
             if (has_next && nxt != w_cur) w_issue(nxt);
           }
           bulk_wait_read_all();
