@@ -140,6 +140,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_mlp(TcParams p) {
 #pragma unroll
   for (int i = 0; i < H / 32; ++i) head_acc[i] = 0.f;
   float bo_acc = 0.f;
+  const uint64_t pol_z = policy_evict_first();  // z stash: written once, read once by the next kernel
   constexpr bool kSplit = H >= 128;  // N halves need whole 64-column blocks for the MN-major dX operand
   constexpr int NH = kSplit ? H / 2 : H;
   const uint32_t idesc_f = idesc_bf16(128, NH, 0, 0);
@@ -243,18 +244,17 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_mlp(TcParams p) {
           float z[32];
 #pragma unroll
           for (int i = 0; i < 32; ++i) z[i] = __uint_as_float(v[i]) + sBias[l * H + cb * 32 + i];
-          if (MODE == 1) {  // z_l (fp16, chunk-major) for swish' in the backward
+          if (MODE == 1) {  // z_l (fp16) for swish' in the backward: [16-column chunk][row][32 B]
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              uint32_t h4[4];
+            for (int qq = 0; qq < 2; ++qq) {
+              uint32_t h8[8];
 #pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                __half2 hh = __floats2half2_rn(z[8 * q + 2 * e], z[8 * q + 2 * e + 1]);
-                h4[e] = *reinterpret_cast<uint32_t *>(&hh);
+              for (int e = 0; e < 8; ++e) {
+                __half2 hh = __floats2half2_rn(z[16 * qq + 2 * e], z[16 * qq + 2 * e + 1]);
+                h8[e] = *reinterpret_cast<uint32_t *>(&hh);
               }
-              uint4 *dst = reinterpret_cast<uint4 *>(p.zstash) +
-                           ((((size_t)l * p.n_tiles + tile) * (H / 8) + (cb * 4 + q)) * 128 + row);
-              *dst = make_uint4(h4[0], h4[1], h4[2], h4[3]);
+              st_global_v8_hint(p.zstash + ((((size_t)l * p.n_tiles + tile) * (H / 16) + (cb * 2 + qq)) * 128 + row) * 32,
+                                h8, pol_z);
             }
           }
           if (!last) {
@@ -298,13 +298,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_mlp(TcParams p) {
       // reduce u h_L over the warp's 32 rows), delta_L = u w_o swish'(z)
       const float u_row = valid ? p.u[g / p.n_s] : 0.f;
       {
-        const uint4 *zsrc = reinterpret_cast<const uint4 *>(p.zstash) + (((size_t)(L - 1) * p.n_tiles + tile) * (H / 8)) * 128 + row;
+        const uint8_t *zsrc = p.zstash + (((size_t)(L - 1) * p.n_tiles + tile) * (H / 16) * 128 + row) * 32;
 #pragma unroll 1
         for (int cb = cb_lo; cb < cb_hi; ++cb) {
           float z[32];
+          uint4 zq4[4];
+#pragma unroll
+          for (int qq = 0; qq < 2; ++qq) ld_global_v8_hint(zsrc + (size_t)(cb * 2 + qq) * 128 * 32, zq4[2 * qq], zq4[2 * qq + 1], pol_z);
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
-            const uint4 zq = zsrc[(size_t)(cb * 4 + q) * 128];
+            const uint4 zq = zq4[q];
             const uint32_t zz[4] = {zq.x, zq.y, zq.z, zq.w};
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
@@ -384,14 +387,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_mlp(TcParams p) {
           bulk_wait_read_all();
         }
         __syncthreads();
-        const uint4 *zsrc = reinterpret_cast<const uint4 *>(p.zstash) + (((size_t)(l - 1) * p.n_tiles + tile) * (H / 8)) * 128 + row;
+        const uint8_t *zsrc = p.zstash + (((size_t)(l - 1) * p.n_tiles + tile) * (H / 16) * 128 + row) * 32;
 #pragma unroll 1
         for (int cb = cb_lo; cb < cb_hi; ++cb) {
           uint32_t v[32];
           tmem_ld32(tmem_row + cb * 32, v);
           uint4 zq[4];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) zq[q] = zsrc[(size_t)(cb * 4 + q) * 128];
+          for (int qq = 0; qq < 2; ++qq) ld_global_v8_hint(zsrc + (size_t)(cb * 2 + qq) * 128 * 32, zq[2 * qq], zq[2 * qq + 1], pol_z);
           tmem_wait_ld();
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
