@@ -181,6 +181,10 @@ size_t plan_layout(dinr_ctx *c, int64_t n, bool train, bool host_io, Plan &pl, v
   pl.ring = nullptr;
   pl.dwf = pl.dbf = nullptr;
   if (pl.fused) {
+    // the fused kernels work in pixel groups of two 128-sample tiles: the stash (and the dW
+    // kernels over it) cover whole groups; the tile past an odd tile count holds only invalid
+    // samples, whose delta is exactly zero, so it adds nothing to dW / db
+    pl.n_tiles = 2 * ((pl.nsamp + 255) / 256);
     pl.nf = std::min(std::min(L, 4), 512 / H - (pl.fused2 ? 2 : 1));  // <= 4: per-thread db registers
     pl.nu = L - pl.nf;
     pl.dw_layers = pl.nu;

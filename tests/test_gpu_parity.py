@@ -254,3 +254,41 @@ def test_adam_step_parity_and_repack(ctx, dev, O):
     f2 = torch.zeros(200, device=dev)
     D.project(ctx, idx, f2)
     assert torch.equal(f1, f2)
+
+
+# Fused-kernel variants (k_fused2 + k_dw01 / K5): pixel-group layouts (S N_s = 256 or 128, 1 or 2
+# pixels per group), depths (nu = 0, 1, 2 unfused layers), tiny and ragged batches.
+FUSED_SHAPES = [
+    ("fan512", dict(sub_x=1, n_s=256), {}, 7),            # one ray = one group, nu = 2 (k_dw01)
+    ("fan512", dict(sub_x=2, n_s=64), {}, 9),             # two pixels per group
+    ("fan512", dict(sub_x=4, n_s=32), {}, 5),             # four sub-rays, two pixels per group
+    ("fan512", {}, dict(L=3), 6),                         # nu = 1: K5 with layer-0 feature recompute
+    ("fan512", {}, dict(L=2), 6),                         # nu = 0: every dW fused
+    ("cone512", dict(n_s=64), dict(C=64, L=4), 3),        # cone, 2 x 2 sub-rays, H = 128
+    ("fan512", {}, {}, 1),                                # a single pixel (ragged last group)
+]
+
+
+@pytest.mark.parametrize("case", range(len(FUSED_SHAPES)))
+def test_fused_path_shapes(ctx, dev, O, case):
+    name, over, fover, n = FUSED_SHAPES[case]
+    g, th, t, f, B, prm = setup_case(ctx, dev, name, over, fover, "bf16", "beer")
+    kind, _ = D.train_path(ctx, n)
+    assert kind == 2  # the two-stream fused kernel
+    idx = synth.pixel_batch(name, n, seed=21 + case, **over)
+    S = g["sub_x"] * g["sub_z"]
+    fhat = torch.zeros(n, device=dev)
+    psub = torch.zeros(n * S, device=dev)
+    D.project(ctx, torch.tensor(idx, device=dev), fhat, psub)
+    rf, rp, rc = O.project(g, th, t, f, B, prm, idx)
+    assert rel_linf(fhat.cpu().numpy(), rf) <= 2e-3
+    y, _, _ = O.project_exact(g, th, t, synth.phantom(name), idx, "beer")
+    y = y.astype(np.float32)
+    P = synth.param_count(f["C"], f["L"])
+    grad = torch.zeros(P + 1, device=dev)
+    D.project_and_grad(ctx, torch.tensor(idx, device=dev), torch.tensor(y, device=dev), grad)
+    torch.cuda.synchronize()
+    ref, rc = O.project_and_grad(g, th, t, f, B, prm, idx, y)
+    got = grad.cpu().numpy()
+    assert max(tensor_errs(got[:P], ref[:P], f["C"], f["L"])) <= 1e-2
+    assert abs(got[P] - ref[P]) <= 1e-2 * abs(ref[P])
