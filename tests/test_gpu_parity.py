@@ -292,3 +292,21 @@ def test_fused_path_shapes(ctx, dev, O, case):
     got = grad.cpu().numpy()
     assert max(tensor_errs(got[:P], ref[:P], f["C"], f["L"])) <= 1e-2
     assert abs(got[P] - ref[P]) <= 1e-2 * abs(ref[P])
+
+
+@pytest.mark.parametrize("name", ["fan512", "cone512"])
+def test_training_step_is_deterministic(ctx, dev, name):
+    """Every reduction has a fixed order (per-CTA partials, fixed-order assembly): the same step
+    twice gives bit-identical gradients and loss."""
+    over = dict(n_s=32) if name == "cone512" else {}
+    g, th, t, f, B, prm = setup_case(ctx, dev, name, over, {}, "bf16", "beer")
+    n = 257
+    idx = torch.tensor(synth.pixel_batch(name, n, seed=31, **over), device=dev)
+    y = torch.tensor(synth.synthetic_y(n, 1.0), device=dev)
+    P = synth.param_count(f["C"], f["L"])
+    g1 = torch.zeros(P + 1, device=dev)
+    g2 = torch.zeros(P + 1, device=dev)
+    D.project_and_grad(ctx, idx, y, g1)
+    D.project_and_grad(ctx, idx, y, g2)
+    torch.cuda.synchronize()
+    assert torch.equal(g1, g2)
