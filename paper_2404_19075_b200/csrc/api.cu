@@ -475,7 +475,6 @@ dinr_status tc_forward(dinr_ctx *c, const Plan &pl, int mode, cudaStream_t st) {
 dinr_status launch_dw01(dinr_ctx *c, const Plan &pl, cudaStream_t st) {
   Dw01Params p{};
   p.dstash = pl.dstash;
-  p.fstash = pl.hstash;  // slot of layer 0: the GRFF feature tiles stored by k_fused2
   p.n_tiles = pl.n_tiles;
   p.nsamp = pl.nsamp;
   p.rec32 = pl.rec32;

@@ -2,11 +2,13 @@
 // with both layer inputs recomputed on chip instead of stashed in HBM:
 //   dW_0 = sum delta_0^T gamma(x),      db_0 = sum delta_0          (eq:partiald)
 //   dW_1 = sum delta_1^T h_0,           db_1 = sum delta_1,    h_0 = swish(W_0 gamma(x) + b_0)
-// gamma(x) is the fused kernel's own layer-0 operand tile (bulk-stored by its copy warp), h_0 is
-// recomputed by one forward MMA with the same 0.5-prescaled bf16 W_0 image, bias MMA step and
-// packed-bf16 Swish, so it equals, bit for bit, what the fused kernel used; h_0 is never stored.
-//   warp 0: bulk loads (F double-buffered, delta_0 / delta_1 one slot each); warp 1: MMA issuer;
-//   warps 2..2+4 NQ: thread = (TMEM lane / sample row, column part): y -> h_0 tile.
+// Both layer inputs are recomputed on chip with the fused kernel's own code and rounding, so they
+// equal, bit for bit, what it used: gamma(x) from the ray records (k_features.cuh), h_0 by one
+// forward MMA with the same 0.5-prescaled bf16 W_0 image, bias MMA step and packed-bf16 Swish.
+// Only delta_0 and delta_1 come from HBM.
+//   warp 0: bulk loads of delta_0 / delta_1 (one slot each); warp 1: MMA issuer;
+//   warps 2-9: thread = (TMEM lane / sample row, column half): y -> h_0 tile (Swish);
+//   warps 10-17: thread = (sample row, frequency half): gamma(x) of the next tile -> F (2 buffers).
 // TMEM: y [0, H), dW_0 [H, 2H), dW_1 [2H, 3H), db_0 / db_1 at 3H / 3H + 16 (ones-MMA, column 0).
 #pragma once
 #include "internal.cuh"
@@ -17,7 +19,6 @@ namespace dinr {
 
 struct Dw01Params {
   const uint8_t *dstash;  // [nu][n_tiles] SW128 images of delta_l
-  const uint8_t *fstash;  // [n_tiles] SW128 images of gamma(x) (layer 0's input)
   int64_t n_tiles, nsamp;
   const float4 *rec32;
   Jitter jit;
@@ -30,9 +31,10 @@ struct Dw01Params {
 
 template <int H>
 struct Dw01Layout {
-  static constexpr int NQ = 4;             // column parts per sample row
-  static constexpr int NFW = 4 * NQ;       // feature / Swish warps
-  static constexpr int NT = 64 + 32 * NFW;
+  static constexpr int NQ = 2;             // column parts per sample row (Swish warps)
+  static constexpr int NFW = 4 * NQ;       // Swish warps
+  static constexpr int NFE = 8;            // GRFF feature warps
+  static constexpr int NT = 64 + 32 * (NFW + NFE);
   static constexpr uint32_t TILE = H * 256u;
   static constexpr int NST = 2;  // delta slots: slot l holds delta_l of the current tile
   static constexpr uint32_t ONES_K = 128 * 32;  // no-swizzle [128][16]: columns 0, 1 = 1 (bias MMA)
@@ -61,7 +63,7 @@ __global__ void __launch_bounds__(Dw01Layout<H>::NT, 1) k_dw01(Dw01Params p) {
   float4 *sB4 = reinterpret_cast<float4 *>(sOnesN + LY::ONES_N);
   uint64_t *bars = reinterpret_cast<uint64_t *>(sB4 + C);
   uint64_t *full = bars, *empty = bars + LY::NST;          // delta stages
-  //   fbar[b] (tx)      F(t) landed in slot b = t % 2
+  //   fbar[b] (NFE warps) F(t) written in slot b = t % 2
   //   f_free[b] (commit) y(t) and dW_0(t) have read F slot b
   //   y_full (commit)   y(t) in TMEM          -> Swish(t)
   //   y_free (NFW warps) Swish(t) loaded y(t) -> y(t+1) MMA may overwrite it
@@ -82,7 +84,7 @@ __global__ void __launch_bounds__(Dw01Layout<H>::NT, 1) k_dw01(Dw01Params p) {
       mbar_init(&empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
-      mbar_init(&fbar[b], 1);
+      mbar_init(&fbar[b], LY::NFE);
       mbar_init(&f_free[b], 1);
     }
     mbar_init(y_full, 1);
@@ -95,6 +97,7 @@ __global__ void __launch_bounds__(Dw01Layout<H>::NT, 1) k_dw01(Dw01Params p) {
   }
   for (int i = tid; i < (int)(LY::ONES_K + LY::BIAS_B) / 4; i += LY::NT) reinterpret_cast<uint32_t *>(sOnesK)[i] = 0u;
   for (int i = tid; i < (int)LY::ONES_N / 4; i += LY::NT) reinterpret_cast<uint32_t *>(sOnesN)[i] = 0x3F803F80u;
+  for (int i = tid; i < C; i += LY::NT) sB4[i] = reinterpret_cast<const float4 *>(p.B)[i];
   __syncthreads();
   for (int i = tid; i < 128; i += LY::NT) {
     *reinterpret_cast<__nv_bfloat16 *>(sOnesK + nosw16_offset(i, 0)) = __float2bfloat16_rn(1.f);
@@ -118,15 +121,11 @@ __global__ void __launch_bounds__(Dw01Layout<H>::NT, 1) k_dw01(Dw01Params p) {
   for (int64_t t = split; t < p.n_tiles; t += ks) ++count;
 
   if (warp == 0) {
-    if (lane == 0) {  // ------------------------------------------- F / delta loads (+ W_0 once)
+    if (lane == 0) {  // ------------------------------------------- delta loads (+ W_0 once)
       mbar_arrive_expect_tx(w_bar, H * H * 2);
       bulk_g2s(sW0, p.wpack_half, H * H * 2, w_bar);
       int it = 0;
       for (int64_t t = split; t < p.n_tiles; t += ks, ++it) {
-        const int fb = it & 1;
-        if (it >= 2) mbar_wait_sleep(&f_free[fb], ((it - 2) >> 1) & 1, 1000);
-        mbar_arrive_expect_tx(&fbar[fb], TILE);
-        bulk_g2s(sF + fb * TILE, p.fstash + (size_t)t * TILE, TILE, &fbar[fb]);
         for (int l = 0; l < 2; ++l) {
           if (it >= 1) mbar_wait_sleep(&empty[l], (it - 1) & 1, 1000);
           mbar_arrive_expect_tx(&full[l], TILE);
@@ -181,8 +180,36 @@ __global__ void __launch_bounds__(Dw01Layout<H>::NT, 1) k_dw01(Dw01Params p) {
       }
       umma_commit(done);
     }
+  } else if (warp >= 2 + LY::NFW) {
+    // --------------------------------------------------------------- GRFF feature warps
+    const int row = ((warp & 3) << 5) | lane, fh = (warp - 2 - LY::NFW) >> 2;  // frequency half
+    const uint32_t f_base = smem_u32(sF);
+    constexpr int NFC = (C / 2) / 8;
+    int it = 0;
+    RayRec rr = grff_fetch(p.rec32, (int64_t)split * 128 + row, p.lg_ns, split < p.n_tiles && (int64_t)split * 128 + row < p.nsamp);
+    for (int64_t t = split; t < p.n_tiles; t += ks, ++it) {
+      const int64_t g = t * 128 + row;
+      const float4 rb = grff_coords_from(rr, g, p.lg_ns, p.n_s, g < p.nsamp, p.jit);
+      const int64_t gn = (t + ks) * 128 + row;  // next tile's ray record, in flight meanwhile
+      rr = grff_fetch(p.rec32, gn, p.lg_ns, t + ks < p.n_tiles && gn < p.nsamp);
+      uint32_t pc[NFC][4], ps[NFC][4];
+#pragma unroll
+      for (int fc = 0; fc < NFC; ++fc) grff8(sB4, fh * (C / 2) + 8 * fc, rb, pc[fc], ps[fc]);
+      const int fb = it & 1;
+      if (it >= 2) mbar_wait_sleep(&f_free[fb], ((it - 2) >> 1) & 1, 1000);  // y(t-2), dW_0(t-2) read it
+      const uint32_t fbase = f_base + fb * TILE;
+#pragma unroll
+      for (int fc = 0; fc < NFC; ++fc) {
+        const int c0 = fh * (C / 2) + 8 * fc;
+        st_shared_v4(fbase + sw128_offset(row, c0, 128), pc[fc][0], pc[fc][1], pc[fc][2], pc[fc][3]);
+        st_shared_v4(fbase + sw128_offset(row, C + c0, 128), ps[fc][0], ps[fc][1], ps[fc][2], ps[fc][3]);
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&fbar[fb]);
+    }
   } else {
-    // --------------------------------------------------------------- feature / Swish warps
+    // --------------------------------------------------------------- Swish warps
     constexpr int NQ = LY::NQ;
     const int row = ((warp & 3) << 5) | lane, half = (warp - 2) >> 2;  // half = column part 0..NQ-1
     const uint32_t f_base = smem_u32(sF), h_base = smem_u32(sH0);
@@ -224,8 +251,8 @@ __global__ void __launch_bounds__(Dw01Layout<H>::NT, 1) k_dw01(Dw01Params p) {
     }
   }
   __syncwarp();
-  // --------------------------------------------------------------- flush (warps 2-9)
-  if (warp >= 2) {
+  // --------------------------------------------------------------- flush (Swish warps 2-9)
+  if (warp >= 2 && warp < 2 + LY::NFW) {
     if (count > 0) {
       mbar_wait_sleep(done, 0, 1000);
       tc_fence_after();

@@ -256,9 +256,9 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
               bulk_s2g_hint(ring_h(s, l - nu), sA, TILE, pol_keep);
               bulk_commit();
               bulk_wait_read_all();
-            } else if ((l > 0 && !p.dw01) || (l == 0 && p.dw01)) {
-              // input of an unfused layer for the dW kernel (K5 recomputes layer 0's features;
-              // k_dw01 takes layer 0's and recomputes layer 1's)
+            } else if (l > 0 && !p.dw01) {
+              // input of an unfused layer for K5 (which recomputes layer 0's features; k_dw01
+              // recomputes both of its inputs)
               bulk_s2g_hint(p.hstash + ((size_t)l * p.n_tiles + tile) * TILE, sA, TILE, pol_stream);
               bulk_commit();
               bulk_wait_read_all();
