@@ -104,6 +104,7 @@ struct Plan {
   // fused training path (k_fused): nf top layers' dW in TMEM, nu = L - nf through K5
   bool fused, fused2;  // fused2: two concurrent tile streams (k_fused2)
   bool dw01;           // layers 0 and 1 unfused, both inputs recomputed by k_dw01 (no input stash)
+  bool feat0;          // the dW GEMM recomputes layer 0's input (needs N_s a power of two)
   int nf, nu, grid_f, dw_layers;
   uint8_t *ring;
   float *dwf, *dbf;
@@ -176,6 +177,9 @@ size_t plan_layout(dinr_ctx *c, int64_t n, bool train, bool host_io, Plan &pl, v
   pl.fused = train && use_fused(c);
   pl.fused2 = pl.fused && use_fused2(c);
   pl.dw01 = false;
+  // layer 0's features recomputed by the dW GEMM instead of stashed: on the fused path (for the
+  // split path, H = 256, the recompute of 128 frequencies costs more than the stash traffic)
+  pl.feat0 = pl.fused;
   pl.nf = pl.nu = pl.grid_f = 0;
   pl.dw_layers = L;
   pl.ring = nullptr;
@@ -333,6 +337,7 @@ dinr_status launch_tc_mlp(dinr_ctx *c, const Plan &pl, int mode, cudaStream_t st
   p.zstash = pl.zstash;
   p.head_part = pl.head_part;
   p.n_tiles = pl.n_tiles;
+  p.stash_feat = pl.feat0 ? 0 : 1;
   size_t smem = TcLayout<H>::smem_bytes(c->L, p.resident != 0);
   if (mode == 2) {
     dinr_status s = set_smem(c, k_tc_mlp<H, 2>, smem);
@@ -366,7 +371,7 @@ dinr_status launch_tc_dw(dinr_ctx *c, const Plan &pl, cudaStream_t st) {
   p.nmb = pl.nmb;
   p.dw_part = pl.dw_part;
   p.db_part = pl.db_part;
-  p.feat0 = pl.fused ? 1 : 0;  // the fused kernels do not stash layer 0's input
+  p.feat0 = pl.feat0 ? 1 : 0;  // layer 0's input (GRFF features) recomputed, not stashed
   p.rec32 = pl.rec32;
   p.B = c->d_B;
   p.n_s = c->geom.samples_per_ray;

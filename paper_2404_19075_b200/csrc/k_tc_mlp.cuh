@@ -37,6 +37,7 @@ struct TcParams {
   uint8_t *hstash, *dstash, *zstash;
   float *head_part;  // [gridDim.x][H+1]
   int64_t n_tiles;
+  int stash_feat;  // MODE 1: store layer 0's input tile (0: the dW GEMM recomputes the features)
   // N4 inference: samples are voxel centres of vg, outputs per voxel to vout (forward only)
   int grid_mode;
   VoxGrid vg;
@@ -199,7 +200,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_mlp(TcParams p) {
       fence_proxy_async_smem();
       tc_fence_before();
       __syncthreads();
-      if (MODE == 1 && tid == 0) {  // layer 0's input for the dW GEMM
+      if (MODE == 1 && p.stash_feat && tid == 0) {  // layer 0's input for the dW GEMM (unless it recomputes it)
         bulk_s2g(p.hstash + ((size_t)0 * p.n_tiles + tile) * A_BYTES, sA, A_BYTES);
         bulk_commit();
       }
