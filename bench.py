@@ -212,6 +212,8 @@ def main():
     ap.add_argument("--batch", type=int, default=0, help="pixels per GPU per step (default: workload's)")
     ap.add_argument("--cpu-baseline-seconds", type=float, default=15.0)
     ap.add_argument("--combine", default="beer", choices=["beer", "linear"])
+    ap.add_argument("--strong", action="store_true",
+                    help="strong scaling: the workload's batch is the global batch, split over the ranks")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
@@ -245,6 +247,8 @@ def main():
     H = 2 * C_
     S, ns = g["sub_x"] * g["sub_z"], g["n_s"]
     n = args.batch or synth.WORKLOADS[name]["batch"]
+    if args.strong:
+        n = max(1, (n + world - 1) // world)  # fixed global batch (SURVEY 8(e) strong scaling)
     P = synth.param_count(C_, L)
     B = torch.tensor(synth.grff_matrix(C_, f["sigma_t"], f["sigma_s"]), device=dev)
     params = torch.tensor(synth.init_params(C_, L), device=dev)
@@ -343,6 +347,13 @@ def main():
         e2e_ms.append(1e3 * (time.perf_counter() - t0))
     e2e_total = sum(e2e_ms)
 
+    # replicas stay identical after allreduce + Adam: compare the parameters
+    replicas_equal = True
+    if world > 1:
+        gathered = [torch.empty_like(params) for _ in range(world)]
+        dist.all_gather(gathered, params)
+        replicas_equal = all(torch.equal(gathered[0], x) for x in gathered[1:])
+
     # max over ranks
     vals = torch.tensor([total_ms, e2e_total], dtype=torch.float64, device=dev)
     if world > 1:
@@ -387,7 +398,8 @@ def main():
             base_rate, base_px, base_dt = oracle_rate(name, budget_s=args.cpu_baseline_seconds)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong" if args.strong else "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": name, "pixels_per_gpu": n, "sub_rays": S, "samples_per_ray": ns,
                        "mlp": f"{L}x{H}", "params": P, "samples_per_step": samples_per_step,
@@ -406,6 +418,7 @@ def main():
                     "d2h_bytes_per_step": (P + 1) * 4},
             "gpu_launches": launches,
             "clocks": clocks,
+            "replicas_equal": replicas_equal,
         }
         print(json.dumps(line), flush=True)
     D.destroy(ctx)
