@@ -14,7 +14,8 @@
  *   - The context owns the per-view table, packed bf16 weights, scratch (ray records,
  *     per-chunk ray sums, upstream gradients, activation stashes, gradient partials),
  *     timing events and the NCCL communicator.  One context per device per process; a
- *     context is not thread-safe (serialize calls on it).
+ *     context is not thread-safe (serialize calls on it), and its calls must be ordered on
+ *     one stream (or synchronized between streams): consecutive calls reuse the same scratch.
  *   - Scratch grows on demand with the largest n seen.  Growth allocates; pre-size it with
  *     one untimed call before capturing a CUDA graph.
  * Errors:
