@@ -298,6 +298,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_mlp(TcParams p) {
       // top layer from the stashed z_{L-1}: h_L = swish(z) for the head gradients (transpose-
       // reduce u h_L over the warp's 32 rows), delta_L = u w_o swish'(z)
       const float u_row = valid ? p.u[g / p.n_s] : 0.f;
+      constexpr uint32_t kZTile = 128u * H * 2u;  // one tile of fp16 z
+      if (tid == 0 && L >= 2)  // z_{L-2} is read after the first dX: bring it to L2 now
+        bulk_prefetch_l2(p.zstash + ((size_t)(L - 2) * p.n_tiles + tile) * kZTile, kZTile);
       {
         const uint8_t *zsrc = p.zstash + (((size_t)(L - 1) * p.n_tiles + tile) * (H / 16) * 128 + row) * 32;
 #pragma unroll 1
@@ -363,6 +366,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_mlp(TcParams p) {
         if (tid == 0) {
           uint32_t wl = w_ready(l);
           tc_fence_after();
+          // z of the next step (or the next tile's top layer) into L2 while this step runs
+          if (l >= 2)
+            bulk_prefetch_l2(p.zstash + ((size_t)(l - 2) * p.n_tiles + tile) * kZTile, kZTile);
+          else if (more_tiles)
+            bulk_prefetch_l2(p.zstash + ((size_t)(L - 1) * p.n_tiles + tile + gridDim.x) * kZTile, kZTile);
           for (int half = 0; half < 2; ++half) {  // input columns [half NH, (half+1) NH)
             if (half == 0 || kSplit) {
 #pragma unroll 4
