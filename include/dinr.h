@@ -74,7 +74,9 @@ typedef enum { DINR_MIDPOINT = 0, DINR_JITTER = 1 } dinr_sampling;
  *   samples_per_ray N_s: fixed midpoint rule per ray (R8).
  *   Normalization box (R11): x -> (x - rot_center_x)/r, y -> y/r,
  *   z -> (z - (z_lo+z_hi)/2)/((z_hi-z_lo)/2), t -> (t - (t_lo+t_hi)/2)/((t_hi-t_lo)/2);
- *   a zero-width range maps that coordinate to 0.
+ *   a zero-width range maps that coordinate to 0.  NaN z_lo / z_hi: derived from the geometry —
+ *   the detector z extent [-C_z, -C_z + n_rows dz], scaled for cone beam by (sod + r)/(sod + odd)
+ *   (the far side of the FOV cylinder); NaN t_lo / t_hi: the first / last view time.
  * Invariants: sod > 0, odd >= 0, pixel pitches > 0, fov_radius > 0,
  *   fov_radius < sod, sub_x, sub_z >= 1, samples_per_ray >= 32 and a multiple of 32,
  *   n_rows, n_cols >= 1, z_hi >= z_lo, t_hi >= t_lo. */

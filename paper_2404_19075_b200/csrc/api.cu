@@ -779,8 +779,26 @@ dinr_status dinr_set_sampling(dinr_ctx *c, dinr_sampling mode, uint64_t seed, ui
   return DINR_OK;
 }
 
-dinr_status dinr_set_geometry(dinr_ctx *c, const dinr_geometry *g, const double *theta, const double *t, int64_t M) {
-  if (!c || !g || !theta || !t) return c ? fail(c, DINR_EINVAL, "null argument") : DINR_EINVAL;
+dinr_status dinr_set_geometry(dinr_ctx *c, const dinr_geometry *g_in, const double *theta, const double *t, int64_t M) {
+  if (!c || !g_in || !theta || !t) return c ? fail(c, DINR_EINVAL, "null argument") : DINR_EINVAL;
+  // NaN normalization ranges are derived (R11): detector z extent (cone: scaled to the far side of
+  // the FOV cylinder), first / last view time
+  dinr_geometry gd = *g_in;
+  if (std::isnan(gd.z_lo) || std::isnan(gd.z_hi)) {
+    double zlo = -gd.offset_cz, zhi = -gd.offset_cz + (double)gd.n_rows * gd.pixel_dz;
+    if (gd.beam == DINR_CONE) {
+      const double mag_far = (gd.sod + gd.fov_radius) / (gd.sod + gd.odd);
+      zlo *= mag_far;
+      zhi *= mag_far;
+    }
+    if (std::isnan(gd.z_lo)) gd.z_lo = zlo;
+    if (std::isnan(gd.z_hi)) gd.z_hi = zhi;
+  }
+  if (M >= 1 && (std::isnan(gd.t_lo) || std::isnan(gd.t_hi))) {
+    if (std::isnan(gd.t_lo)) gd.t_lo = t[0];
+    if (std::isnan(gd.t_hi)) gd.t_hi = t[M - 1];
+  }
+  const dinr_geometry *g = &gd;
   if (g->beam < 0 || g->beam > 2) return fail(c, DINR_EINVAL, "beam must be 0 (parallel), 1 (fan) or 2 (cone)");
   if (g->n_rows < 1 || g->n_cols < 1) return fail(c, DINR_EINVAL, "n_rows, n_cols must be >= 1");
   if (g->sub_x < 1 || g->sub_z < 1 || g->sub_x * g->sub_z > kMaxS)

@@ -310,3 +310,20 @@ def test_training_step_is_deterministic(ctx, dev, name):
     D.project_and_grad(ctx, idx, y, g2)
     torch.cuda.synchronize()
     assert torch.equal(g1, g2)
+
+
+@pytest.mark.parametrize("name", ["fan512", "cone4d512"])
+def test_nan_normalization_box_is_derived(ctx, dev, name):
+    """NaN z_lo / z_hi / t_lo / t_hi are derived from the geometry exactly as the input recipe
+    derives them (R11): same projections bit for bit."""
+    over = dict(n_s=32) if name.startswith("cone") else {}
+    g, th, t, f, B, prm = setup_case(ctx, dev, name, over, {}, "bf16", "beer")
+    idx = torch.tensor(synth.pixel_batch(name, 64, seed=41, **over), device=dev)
+    a = torch.zeros(64, device=dev)
+    D.project(ctx, idx, a)
+    gn = dict(g, z_lo=float("nan"), z_hi=float("nan"), t_lo=float("nan"), t_hi=float("nan"))
+    D.set_geometry(ctx, gn, th, t)
+    b = torch.zeros(64, device=dev)
+    D.project(ctx, idx, b)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
