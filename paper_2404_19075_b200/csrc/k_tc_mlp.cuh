@@ -242,17 +242,27 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_mlp(TcParams p) {
           uint32_t v[32];
           tmem_ld32(tmem_row + cb * 32, v);
           tmem_wait_ld();
-          float z[32];
+          float z[32], sg[32];  // pre-activation and its sigmoid (one tanh per element)
 #pragma unroll
-          for (int i = 0; i < 32; ++i) z[i] = __uint_as_float(v[i]) + sBias[l * H + cb * 32 + i];
-          if (MODE == 1) {  // z_l (fp16) for swish' in the backward: [16-column chunk][row][32 B]
+          for (int i = 0; i < 32; ++i) {
+            z[i] = __uint_as_float(v[i]) + sBias[l * H + cb * 32 + i];
+            sg[i] = 0.5f + 0.5f * tanh_approx(0.5f * z[i]);
+          }
+          if (MODE == 1) {  // backward state, [16-column chunk][row][32 B]: swish'(z_l) as bf16 for the
+                            // hidden layers (no tanh in the backward), z_{L-1} as fp16 for the top layer
 #pragma unroll
             for (int qq = 0; qq < 2; ++qq) {
               uint32_t h8[8];
 #pragma unroll
               for (int e = 0; e < 8; ++e) {
-                __half2 hh = __floats2half2_rn(z[16 * qq + 2 * e], z[16 * qq + 2 * e + 1]);
-                h8[e] = *reinterpret_cast<uint32_t *>(&hh);
+                const int i0 = 16 * qq + 2 * e;
+                if (last) {
+                  __half2 hh = __floats2half2_rn(z[i0], z[i0 + 1]);
+                  h8[e] = *reinterpret_cast<uint32_t *>(&hh);
+                } else {  // swish'(z) = s (1 + z (1 - s))
+                  h8[e] = pack_bf16x2(sg[i0] * (1.f + z[i0] * (1.f - sg[i0])),
+                                      sg[i0 + 1] * (1.f + z[i0 + 1] * (1.f - sg[i0 + 1])));
+                }
               }
               st_global_v8_hint(p.zstash + ((((size_t)l * p.n_tiles + tile) * (H / 16) + (cb * 2 + qq)) * 128 + row) * 32,
                                 h8, pol_z);
@@ -263,12 +273,15 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_mlp(TcParams p) {
             for (int q = 0; q < 4; ++q) {
               uint32_t w4[4];
 #pragma unroll
-              for (int e = 0; e < 4; ++e) w4[e] = pack_bf16x2(swish_f(z[8 * q + 2 * e]), swish_f(z[8 * q + 2 * e + 1]));
+              for (int e = 0; e < 4; ++e) {
+                const int i0 = 8 * q + 2 * e;
+                w4[e] = pack_bf16x2(z[i0] * sg[i0], z[i0 + 1] * sg[i0 + 1]);  // swish(z) = z s
+              }
               st_shared_v4(a_base + sw128_offset(row, cb * 32 + 8 * q, 128), w4[0], w4[1], w4[2], w4[3]);
             }
           } else {
 #pragma unroll
-            for (int i = 0; i < 32; ++i) mu_acc += sWo[cb * 32 + i] * swish_f(z[i]);
+            for (int i = 0; i < 32; ++i) mu_acc += sWo[cb * 32 + i] * (z[i] * sg[i]);
           }
         }
         if (!last) fence_proxy_async_smem();
@@ -410,11 +423,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_mlp(TcParams p) {
             const uint32_t zz[4] = {zq[q].x, zq[q].y, zq[q].z, zq[q].w};
             uint32_t w4[4];
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              __half2 hh = *reinterpret_cast<const __half2 *>(&zz[e]);
-              float2 zf = __half22float2(hh);
+            for (int e = 0; e < 4; ++e) {  // delta = e swish'(z), swish' stashed as bf16 by the forward
               int i0 = 8 * q + 2 * e;
-              w4[e] = pack_bf16x2(__uint_as_float(v[i0]) * dswish_f(zf.x), __uint_as_float(v[i0 + 1]) * dswish_f(zf.y));
+              w4[e] = pack_bf16x2(__uint_as_float(v[i0]) * bf16lo(zz[e]), __uint_as_float(v[i0 + 1]) * bf16hi(zz[e]));
             }
             st_shared_v4(a_base + sw128_offset(row, cb * 32 + 8 * q, 128), w4[0], w4[1], w4[2], w4[3]);
           }
