@@ -1,15 +1,18 @@
 // k_dw01.cuh -- weight gradients of layers 0 and 1 after the fused kernel (fan512 path, nu = 2),
-// with both layer inputs recomputed on chip instead of stashed in HBM:
+// with both layer inputs and delta_0 recomputed on chip instead of stashed in HBM:
 //   dW_0 = sum delta_0^T gamma(x),      db_0 = sum delta_0          (eq:partiald)
 //   dW_1 = sum delta_1^T h_0,           db_1 = sum delta_1,    h_0 = swish(W_0 gamma(x) + b_0)
-// Both layer inputs are recomputed on chip with the fused kernel's own code and rounding, so they
-// equal, bit for bit, what it used: gamma(x) from the ray records (k_features.cuh), h_0 by one
-// forward MMA with the same 0.5-prescaled bf16 W_0 image, bias MMA step and packed-bf16 Swish.
-// Only delta_0 and delta_1 come from HBM.
-//   warp 0: bulk loads of delta_0 / delta_1 (one slot each); warp 1: MMA issuer;
-//   warps 2-9: thread = (TMEM lane / sample row, column half): y -> h_0 tile (Swish);
+//   delta_0 = (delta_1 W_1) swish'(z_0)                             (the chain rule's last dX step)
+// Everything is recomputed with the fused kernel's own code and rounding, so it equals, bit for
+// bit, what that kernel would have formed: gamma(x) from the ray records (k_features.cuh), h_0 and
+// s2_0 = 2 swish'(z_0) from one forward MMA with the same 0.5-prescaled bf16 W_0 image, bias MMA
+// step and packed-bf16 Swish, e_0 = delta_1 W_1 / 2 by the same dX MMA.  Only delta_1 comes from HBM.
+//   warp 0: bulk loads (W_0, W_1 once; delta_1 per tile, the next tile prefetched into L2);
+//   warp 1: MMA issuer, per tile t: e_0(t), dW_1(t), y(t+1), dW_0(t);
+//   warps 2-9: thread = (TMEM lane / sample row, column half): y -> h_0 tile and s2_0 (registers),
+//              then e_0 -> delta_0 tile, both through the one HD tile buffer;
 //   warps 10-17: thread = (sample row, frequency half): gamma(x) of the next tile -> F (2 buffers).
-// TMEM: y [0, H), dW_0 [H, 2H), dW_1 [2H, 3H), db_0 / db_1 at 3H / 3H + 16 (ones-MMA, column 0).
+// TMEM: R [0, H) = y(t), then e_0(t); dW_0 [H, 2H), dW_1 [2H, 3H), db_0 / db_1 at 3H / 3H + 16.
 #pragma once
 #include "internal.cuh"
 #include "k_features.cuh"
@@ -17,15 +20,22 @@
 
 namespace dinr {
 
+// waits spin by default (suspended try_waits overslept: +0.19 ms per step on fan512)
+#ifdef DINR_DW01_SLEEP
+#define DW01_WAIT(bar, ph) mbar_wait_sleep(bar, ph, 1000)
+#else
+#define DW01_WAIT(bar, ph) mbar_wait(bar, ph)
+#endif
+
 struct Dw01Params {
-  const uint8_t *dstash;  // [nu][n_tiles] SW128 images of delta_l
+  const uint8_t *dstash;  // [nu][n_tiles] SW128 images of delta_l (only l = 1 is read)
   int64_t n_tiles, nsamp;
   const float4 *rec32;
   Jitter jit;
   const float *B;
   int n_s, lg_ns;
   const float *params;
-  const uint16_t *wpack_half;  // layer 0's W/2 image first
+  const uint16_t *wpack_half;  // W_0 / 2 image, then W_1 / 2
   float *dw_part, *db_part;    // [l][ksplit][128][H], [l][ksplit][128]; ksplit = gridDim.x
 };
 
@@ -36,13 +46,11 @@ struct Dw01Layout {
   static constexpr int NFE = 8;            // GRFF feature warps
   static constexpr int NT = 64 + 32 * (NFW + NFE);
   static constexpr uint32_t TILE = H * 256u;
-  static constexpr int NST = 2;  // delta slots: slot l holds delta_l of the current tile
   static constexpr uint32_t ONES_K = 128 * 32;  // no-swizzle [128][16]: columns 0, 1 = 1 (bias MMA)
   static constexpr uint32_t BIAS_B = H * 32;
   static constexpr uint32_t ONES_N = 2048;      // SW128 K-major [16 rows][64] of ones (db MMA B operand)
-  static size_t smem_bytes() {
-    return 1024 + (size_t)NST * TILE + 3 * TILE + (size_t)H * H * 2 + ONES_K + BIAS_B + ONES_N + (H / 2) * 16 + 256;
-  }
+  // delta_1, F x 2, HD (h_0 then delta_0), W_0, W_1
+  static size_t smem_bytes() { return 1024 + 4 * (size_t)TILE + 2 * (size_t)H * H * 2 + ONES_K + BIAS_B + ONES_N + (H / 2) * 16 + 256; }
 };
 
 template <int H>
@@ -53,25 +61,27 @@ __global__ void __launch_bounds__(Dw01Layout<H>::NT, 1) k_dw01(Dw01Params p) {
   constexpr uint32_t TILE = LY::TILE;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint8_t *sD = smem;                          // NST delta tiles
-  uint8_t *sF = sD + LY::NST * TILE;           // gamma(x) tiles (double-buffered)
-  uint8_t *sH0 = sF + 2 * TILE;                // h_0 tile
-  uint8_t *sW0 = sH0 + TILE;                   // W_0 / 2
-  uint8_t *sOnesK = sW0 + (size_t)H * H * 2;
+  uint8_t *sD1 = smem;                         // delta_1 tile
+  uint8_t *sF = sD1 + TILE;                    // gamma(x) tiles (double-buffered)
+  uint8_t *sHD = sF + 2 * TILE;                // h_0 tile, then delta_0 tile
+  uint8_t *sW0 = sHD + TILE;                   // W_0 / 2
+  uint8_t *sW1 = sW0 + (size_t)H * H * 2;      // W_1 / 2
+  uint8_t *sOnesK = sW1 + (size_t)H * H * 2;
   uint8_t *sBias = sOnesK + LY::ONES_K;
   uint8_t *sOnesN = sBias + LY::BIAS_B;
   float4 *sB4 = reinterpret_cast<float4 *>(sOnesN + LY::ONES_N);
   uint64_t *bars = reinterpret_cast<uint64_t *>(sB4 + C);
-  uint64_t *full = bars, *empty = bars + LY::NST;          // delta stages
-  //   fbar[b] (NFE warps) F(t) written in slot b = t % 2
-  //   f_free[b] (commit) y(t) and dW_0(t) have read F slot b
-  //   y_full (commit)   y(t) in TMEM          -> Swish(t)
-  //   y_free (NFW warps) Swish(t) loaded y(t) -> y(t+1) MMA may overwrite it
-  //   h_full (NFW warps) h_0(t) written       -> dW_1(t)
-  //   h_free (commit)   dW_1(t) read h_0(t)   -> h_0(t+1) may be written
-  uint64_t *fbar = bars + 2 * LY::NST, *f_free = fbar + 2, *y_full = fbar + 4, *y_free = fbar + 5;
-  uint64_t *h_full = fbar + 6, *h_free = fbar + 7, *w_bar = fbar + 8, *done = fbar + 9;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(fbar + 10);
+  //   d1_full (tx)      delta_1(t) landed        d1_free (commit)  e_0(t), dW_1(t) read it
+  //   fbar[b] (NFE)     F(t) in slot b = t % 2   f_free[b] (commit) y(t), dW_0(t) read F slot b
+  //   y_full (commit)   y(t) in R                y_free (NFW)      Swish loaded y(t): e_0(t) may overwrite R
+  //   e_full (commit)   e_0(t) in R              e_free (NFW)      e_0(t) loaded: y(t+1) may overwrite R
+  //   h_full (NFW)      h_0(t) in HD             h_done (commit)   dW_1(t) read h_0(t): delta_0(t) may overwrite
+  //   d0_full (NFW)     delta_0(t) in HD         d0_done (commit)  dW_0(t) read delta_0(t): h_0(t+1) may overwrite
+  uint64_t *d1_full = bars, *d1_free = bars + 1, *fbar = bars + 2, *f_free = bars + 4;
+  uint64_t *y_full = bars + 6, *y_free = bars + 7, *e_full = bars + 8, *e_free = bars + 9;
+  uint64_t *h_full = bars + 10, *h_done = bars + 11, *d0_full = bars + 12, *d0_done = bars + 13;
+  uint64_t *w_bar = bars + 14, *done = bars + 15;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 16);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (warp == 0) {
@@ -79,18 +89,20 @@ __global__ void __launch_bounds__(Dw01Layout<H>::NT, 1) k_dw01(Dw01Params p) {
     tmem_relinquish();
   }
   if (tid == 0) {
-    for (int s = 0; s < LY::NST; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
-    }
+    mbar_init(d1_full, 1);
+    mbar_init(d1_free, 1);
     for (int b = 0; b < 2; ++b) {
       mbar_init(&fbar[b], LY::NFE);
       mbar_init(&f_free[b], 1);
     }
     mbar_init(y_full, 1);
     mbar_init(y_free, LY::NFW);
+    mbar_init(e_full, 1);
+    mbar_init(e_free, LY::NFW);
     mbar_init(h_full, LY::NFW);
-    mbar_init(h_free, 1);
+    mbar_init(h_done, 1);
+    mbar_init(d0_full, LY::NFW);
+    mbar_init(d0_done, 1);
     mbar_init(w_bar, 1);
     mbar_init(done, 1);
     fence_mbar_init();
@@ -115,68 +127,82 @@ __global__ void __launch_bounds__(Dw01Layout<H>::NT, 1) k_dw01(Dw01Params p) {
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t t_y = tmem, t_dw0 = tmem + H, t_dw1 = tmem + 2 * H, t_db0 = tmem + 3 * H, t_db1 = tmem + 3 * H + 16;
+  const uint32_t t_r = tmem, t_dw0 = tmem + H, t_dw1 = tmem + 2 * H, t_db0 = tmem + 3 * H, t_db1 = tmem + 3 * H + 16;
   const int ks = gridDim.x, split = blockIdx.x;
   int count = 0;
   for (int64_t t = split; t < p.n_tiles; t += ks) ++count;
 
   if (warp == 0) {
-    if (lane == 0) {  // ------------------------------------------- delta loads (+ W_0 once)
-      mbar_arrive_expect_tx(w_bar, H * H * 2);
+    if (lane == 0) {  // ------------------------------------------- bulk loads
+      mbar_arrive_expect_tx(w_bar, 2 * H * H * 2);
       bulk_g2s(sW0, p.wpack_half, H * H * 2, w_bar);
+      bulk_g2s(sW1, p.wpack_half + H * H, H * H * 2, w_bar);
+      const uint8_t *d1src = p.dstash + (size_t)p.n_tiles * TILE;  // layer 1's images
       int it = 0;
       for (int64_t t = split; t < p.n_tiles; t += ks, ++it) {
-        for (int l = 0; l < 2; ++l) {
-          if (it >= 1) mbar_wait_sleep(&empty[l], (it - 1) & 1, 1000);
-          mbar_arrive_expect_tx(&full[l], TILE);
-          bulk_g2s(sD + l * TILE, p.dstash + ((size_t)l * p.n_tiles + t) * TILE, TILE, &full[l]);
-        }
+        if (t + ks < p.n_tiles) bulk_prefetch_l2(d1src + (size_t)(t + ks) * TILE, TILE);
+        if (it >= 1) DW01_WAIT(d1_free, (it - 1) & 1);
+        mbar_arrive_expect_tx(d1_full, TILE);
+        bulk_g2s(sD1, d1src + (size_t)t * TILE, TILE, d1_full);
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ------------------------------------------- MMA issuer
-      const uint32_t idf = idesc_bf16(128, H, 0, 0), idw = idesc_bf16(128, H, 1, 1), idb = idesc_bf16(128, 16, 1, 0);
-      const uint32_t f_base = smem_u32(sF), h_base = smem_u32(sH0), w0 = smem_u32(sW0), on = smem_u32(sOnesN);
+      const uint32_t idf = idesc_bf16(128, H, 0, 0), idx = idesc_bf16(128, H, 0, 1), idw = idesc_bf16(128, H, 1, 1);
+      const uint32_t idb = idesc_bf16(128, 16, 1, 0);
+      const uint32_t f_base = smem_u32(sF), hd = smem_u32(sHD), d1 = smem_u32(sD1), on = smem_u32(sOnesN);
+      const uint32_t w0 = smem_u32(sW0), w1 = smem_u32(sW1);
       mbar_wait(w_bar, 0);
-      auto y_mma = [&](int it) {  // y(t) = gamma(x) W_0^T / 2 + b_0 / 2 into t_y
+      auto y_mma = [&](int it) {  // y(t) = gamma(x) W_0^T / 2 + b_0 / 2 into R
         const uint32_t fbase = f_base + (it & 1) * TILE;
         mbar_wait(&fbar[it & 1], (it >> 1) & 1);
-        if (it > 0) mbar_wait(y_free, (it - 1) & 1);  // Swish(t-1) has loaded its y
+        if (it > 0) mbar_wait(e_free, (it - 1) & 1);  // e_0(t-1) has been loaded from R
         tc_fence_after();
-        umma_bf16(t_y, sdesc_none(smem_u32(sOnesK), 128, 256), sdesc_none(smem_u32(sBias), 128, 256), idf, 0u);
+        umma_bf16(t_r, sdesc_none(smem_u32(sOnesK), 128, 256), sdesc_none(smem_u32(sBias), 128, 256), idf, 0u);
 #pragma unroll
         for (int kk = 0; kk < H / 16; ++kk)
-          umma_bf16(t_y, sdesc_sw128(fbase + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
+          umma_bf16(t_r, sdesc_sw128(fbase + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
                     sdesc_sw128(w0 + (kk >> 2) * (H * 128) + (kk & 3) * 32, 16, 1024), idf, 1u);
         umma_commit(y_full);
       };
       if (count > 0) y_mma(0);
       for (int it = 0; it < count; ++it) {
-        const uint32_t d0 = smem_u32(sD), d1 = d0 + TILE, fbase = f_base + (it & 1) * TILE;
-        mbar_wait(&full[0], it & 1);  // delta_0 of this tile
+        const uint32_t fbase = f_base + (it & 1) * TILE;
+        const uint32_t acc = it > 0 ? 1u : 0u;
+        // e_0(t) = delta_1(t) W_1 / 2 into R (the fused kernel's dX MMA of layer 1)
+#ifndef DINR_DW01_NOD1
+        mbar_wait(d1_full, it & 1);
+#endif
+        mbar_wait(y_free, it & 1);
         tc_fence_after();
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {  // layer 0: operand gamma(x)
-          const uint32_t acc = (it > 0 || kk > 0) ? 1u : 0u;
-          umma_bf16(t_dw0, sdesc_sw128(d0 + kk * 2048, 16384, 1024), sdesc_sw128(fbase + kk * 2048, 16384, 1024), idw,
-                    acc);
-          umma_bf16(t_db0, sdesc_sw128(d0 + kk * 2048, 16384, 1024), sdesc_sw128(on + (kk & 3) * 32, 16, 1024), idb, acc);
-        }
-        umma_commit(&empty[0]);
-        umma_commit(&f_free[it & 1]);
-        if (it + 1 < count) y_mma(it + 1);  // overlaps Swish(t) on the epilogue warps
-        mbar_wait(&full[1], it & 1);  // delta_1
-        mbar_wait(h_full, it & 1);    // h_0 of this tile in sH0
+        for (int kk = 0; kk < H / 16; ++kk)
+          umma_bf16(t_r, sdesc_sw128(d1 + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024), sdesc_sw128(w1 + kk * 2048, H * 128, 1024),
+                    idx, kk > 0 ? 1u : 0u);
+        umma_commit(e_full);
+        // layer 1: dW_1 += delta_1^T h_0, db_1 += delta_1^T 1
+        mbar_wait(h_full, it & 1);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
-          const uint32_t acc = (it > 0 || kk > 0) ? 1u : 0u;
-          umma_bf16(t_dw1, sdesc_sw128(d1 + kk * 2048, 16384, 1024), sdesc_sw128(h_base + kk * 2048, 16384, 1024), idw,
-                    acc);
-          umma_bf16(t_db1, sdesc_sw128(d1 + kk * 2048, 16384, 1024), sdesc_sw128(on + (kk & 3) * 32, 16, 1024), idb, acc);
+          const uint32_t a = (acc || kk > 0) ? 1u : 0u;
+          umma_bf16(t_dw1, sdesc_sw128(d1 + kk * 2048, 16384, 1024), sdesc_sw128(hd + kk * 2048, 16384, 1024), idw, a);
+          umma_bf16(t_db1, sdesc_sw128(d1 + kk * 2048, 16384, 1024), sdesc_sw128(on + (kk & 3) * 32, 16, 1024), idb, a);
         }
-        umma_commit(&empty[1]);
-        umma_commit(h_free);
+        umma_commit(d1_free);
+        umma_commit(h_done);
+        if (it + 1 < count) y_mma(it + 1);  // overlaps the delta_0 epilogue
+        // layer 0: dW_0 += delta_0^T gamma(x), db_0 += delta_0^T 1
+        mbar_wait(d0_full, it & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t a = (acc || kk > 0) ? 1u : 0u;
+          umma_bf16(t_dw0, sdesc_sw128(hd + kk * 2048, 16384, 1024), sdesc_sw128(fbase + kk * 2048, 16384, 1024), idw, a);
+          umma_bf16(t_db0, sdesc_sw128(hd + kk * 2048, 16384, 1024), sdesc_sw128(on + (kk & 3) * 32, 16, 1024), idb, a);
+        }
+        umma_commit(&f_free[it & 1]);
+        umma_commit(d0_done);
       }
       umma_commit(done);
     }
@@ -196,7 +222,7 @@ __global__ void __launch_bounds__(Dw01Layout<H>::NT, 1) k_dw01(Dw01Params p) {
 #pragma unroll
       for (int fc = 0; fc < NFC; ++fc) grff8(sB4, fh * (C / 2) + 8 * fc, rb, pc[fc], ps[fc]);
       const int fb = it & 1;
-      if (it >= 2) mbar_wait_sleep(&f_free[fb], ((it - 2) >> 1) & 1, 1000);  // y(t-2), dW_0(t-2) read it
+      if (it >= 2) DW01_WAIT(&f_free[fb], ((it - 2) >> 1) & 1);  // y(t-2), dW_0(t-2) read it
       const uint32_t fbase = f_base + fb * TILE;
 #pragma unroll
       for (int fc = 0; fc < NFC; ++fc) {
@@ -209,18 +235,19 @@ __global__ void __launch_bounds__(Dw01Layout<H>::NT, 1) k_dw01(Dw01Params p) {
       if (lane == 0) mbar_arrive(&fbar[fb]);
     }
   } else {
-    // --------------------------------------------------------------- Swish warps
+    // --------------------------------------------------------------- Swish / delta_0 warps
     constexpr int NQ = LY::NQ;
     const int row = ((warp & 3) << 5) | lane, half = (warp - 2) >> 2;  // half = column part 0..NQ-1
-    const uint32_t f_base = smem_u32(sF), h_base = smem_u32(sH0);
-    const uint32_t trow = t_y + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(half * (H / NQ));
+    const uint32_t hd = smem_u32(sHD);
+    const uint32_t trow = t_r + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(half * (H / NQ));
+    constexpr int NHC = H / (16 * NQ);
     int it = 0;
     for (int64_t t = split; t < p.n_tiles; t += ks, ++it) {
-      // h_0 = swish(y_0) of tile t: y = z / 2 from the prescaled MMA, h = y (1 + tanh y)
-      mbar_wait_sleep(y_full, it & 1, 1000);
+      // h_0 = swish(y_0), s2_0 = 2 swish'(z_0) of tile t: y = z / 2 from the prescaled MMA,
+      // h = y (1 + tanh y), s2 = 1 + t + y (1 - t^2) -- the fused kernel's packed-bf16 arithmetic
+      DW01_WAIT(y_full, it & 1);
       tc_fence_after();
-      constexpr int NHC = H / (16 * NQ);
-      uint32_t hpk[NHC][8];
+      uint32_t hpk[NHC][8], s2k[NHC][8];
 #pragma unroll
       for (int hc = 0; hc < NHC; ++hc) {
         uint32_t v[16];
@@ -231,30 +258,65 @@ __global__ void __launch_bounds__(Dw01Layout<H>::NT, 1) k_dw01(Dw01Params p) {
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(y_free);  // y(t+1) may now be computed into TMEM
+      if (lane == 0) mbar_arrive(y_free);  // e_0(t) may now be computed into R
 #pragma unroll
       for (int hc = 0; hc < NHC; ++hc)
 #pragma unroll
-        for (int i = 0; i < 8; ++i) hpk[hc][i] = bf2_fma(hpk[hc][i], bf2_tanh(hpk[hc][i]), hpk[hc][i]);
-      if (it > 0) mbar_wait_sleep(h_free, (it - 1) & 1, 1000);  // dW_1(t-1) has read h_0
+        for (int i = 0; i < 8; ++i) {
+          const uint32_t yb = hpk[hc][i], th = bf2_tanh(yb);
+          const uint32_t w = bf2_fma(th, th ^ kBf2Sign, kBf2One);
+          s2k[hc][i] = bf2_fma(yb, w, bf2_add(th, kBf2One));
+          hpk[hc][i] = bf2_fma(yb, th, yb);
+        }
+#ifndef DINR_DW01_NOHD
+      if (it > 0) DW01_WAIT(d0_done, (it - 1) & 1);
+#endif  // dW_0(t-1) has read delta_0(t-1)
 #pragma unroll
       for (int hc = 0; hc < NHC; ++hc) {
         const int col0 = half * (H / NQ) + hc * 16;
 #pragma unroll
         for (int q = 0; q < 2; ++q)
-          st_shared_v4(h_base + sw128_offset(row, col0 + 8 * q, 128), hpk[hc][4 * q], hpk[hc][4 * q + 1],
-                       hpk[hc][4 * q + 2], hpk[hc][4 * q + 3]);
+          st_shared_v4(hd + sw128_offset(row, col0 + 8 * q, 128), hpk[hc][4 * q], hpk[hc][4 * q + 1], hpk[hc][4 * q + 2],
+                       hpk[hc][4 * q + 3]);
       }
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(h_full);
+      // delta_0 = e_0 s2_0 (e_0 = delta_1 W_1 / 2, s2_0 = 2 swish'(z_0)), rounded as in the fused kernel
+      DW01_WAIT(e_full, it & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int hc = 0; hc < NHC; ++hc) {
+        uint32_t v[16];
+        tmem_ld16(trow + hc * 16, v);
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 8; ++i) hpk[hc][i] = bf2_mul(pack_bf16x2(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1])), s2k[hc][i]);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(e_free);  // y(t+1) may now be computed into R
+#ifndef DINR_DW01_NOHD
+      DW01_WAIT(h_done, it & 1);
+#endif  // dW_1(t) has read h_0(t)
+#pragma unroll
+      for (int hc = 0; hc < NHC; ++hc) {
+        const int col0 = half * (H / NQ) + hc * 16;
+#pragma unroll
+        for (int q = 0; q < 2; ++q)
+          st_shared_v4(hd + sw128_offset(row, col0 + 8 * q, 128), hpk[hc][4 * q], hpk[hc][4 * q + 1], hpk[hc][4 * q + 2],
+                       hpk[hc][4 * q + 3]);
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(d0_full);
     }
   }
   __syncwarp();
   // --------------------------------------------------------------- flush (Swish warps 2-9)
   if (warp >= 2 && warp < 2 + LY::NFW) {
     if (count > 0) {
-      mbar_wait_sleep(done, 0, 1000);
+      DW01_WAIT(done, 0);
       tc_fence_after();
     }
     constexpr int NQ = LY::NQ;

@@ -86,6 +86,8 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // keeps the shared address space
   const int L = p.L, nf = p.nf, nu = L - nf;  // unfused layers 0..nu-1 go through the dW GEMM
+  // lowest backward step run here: with k_dw01, delta_0 = (delta_1 W_1) swish'(z_0) is formed there
+  const int lmin = p.dw01 ? 1 : 0;
   uint8_t *sA0 = smem;
   uint8_t *sXB = sA0 + 2 * LY::A_BYTES;
   uint8_t *sW = sXB + LY::XB;  // W_1..W_{L-1}
@@ -187,7 +189,7 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
             umma_commit(&sa_free[s]);
             if (l == 0 && s == 1) umma_commit(xb_free);  // W_0 retired for this group
           }
-        for (int l = L - 1; l >= 0; --l)
+        for (int l = L - 1; l >= lmin; --l)
           for (int s = 0; s < 2; ++s) {
             const uint32_t a_base = a0_base + s * LY::A_BYTES;
             const bool fused = l >= nu;
@@ -204,7 +206,7 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
                 umma_bf16(dwt, sdesc_sw128(a_base + kk * 2048, 16384, 1024), sdesc_sw128(xb_base + kk * 2048, 16384, 1024),
                           idw, (seen || kk > 0) ? 1u : 0u);
             }
-            if (l > 0) {
+            if (l > lmin) {
               const uint32_t wl = w_base + (uint32_t)(l - 1) * LY::W_LAYER;
 #pragma unroll
               for (int kk = 0; kk < H / 16; ++kk)
@@ -266,7 +268,7 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
             mbar_arrive(&sa_free[s]);
           }
         // ---------------------------------------------------------------- backward
-        for (int l = L - 1; l >= 0; --l)
+        for (int l = L - 1; l >= lmin; --l)
           for (int s = 0; s < 2; ++s) {
             const int64_t tile = 2 * gi + s;
             uint8_t *sA = sA0 + s * LY::A_BYTES;
@@ -426,7 +428,7 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
             // top layer: s2 stays on chip, packed into this thread's already-consumed accumulator
             // columns (acc[s] is idle until the first backward dX MMA)
             tmem_st8(trow + hc * 8, s2k);
-          } else {
+          } else if (l >= lmin) {
             // ring layout [16-column chunk][row][32 B]: one 256-bit store per thread, a warp covers
             // 1 KB contiguous
             st_global_v8_hint(ring_s2(s, l) + ((size_t)(col0 >> 4) * 128 + row) * 32, s2k, pol_keep);
@@ -573,7 +575,7 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
 #pragma unroll
         for (int q = 0; q < 4; ++q) sq[c][q] = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
       }
-      for (int l = L - 1; l >= 0; --l) {
+      for (int l = L - 1; l >= lmin; --l) {
         const bool top = (l == L - 1);
         if (!top) {
           f2_wait(&acc_full[s], accph);
@@ -617,7 +619,7 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
         fence_proxy_async_smem();
         PH2(5);
         f2_arrive_tile(&a_full[s], s);
-        if (l > 0) {  // prefetch s2 of the next backward step
+        if (l > lmin) {  // prefetch s2 of the next backward step
 #pragma unroll
           for (int c = 0; c < NCH; ++c)
 #pragma unroll
@@ -666,7 +668,7 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
         }
         PH2(6);
       }
-      // the l = 0 step (dW MMA or delta_0 store) must retire before A_s is rewritten
+      // the last step (dW MMA or delta stash store) must retire before A_s is rewritten
       f2_wait(&acc_full[s], accph);
       accph ^= 1;
       tc_fence_after();
