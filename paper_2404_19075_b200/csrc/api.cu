@@ -149,7 +149,9 @@ size_t plan_layout(dinr_ctx *c, int64_t n, bool train, bool host_io, Plan &pl, v
   pl.n_tiles = (pl.nsamp + 127) / 128;
   pl.grid_tc = (int)std::max<int64_t>(1, std::min<int64_t>(pl.n_tiles, (int64_t)c->sm_count * tc_occupancy(c)));
   pl.nmb = c->H == 256 ? 2 : 1;
-  pl.ksplit = (int)std::max<int64_t>(1, std::min<int64_t>(pl.n_tiles, (c->sm_count + pl.nmb * c->L - 1) / (pl.nmb * c->L)));
+  // dW GEMM K-split: one wave of nmb * L * ksplit <= sm_count CTAs (one CTA per SM; a second
+  // partial wave would double the kernel time)
+  pl.ksplit = (int)std::max<int64_t>(1, std::min<int64_t>(pl.n_tiles, c->sm_count / (pl.nmb * c->L)));
   pl.ks0 = pl.ks1 = pl.ksplit;
   pl.ksplit_simt = (int)std::max<int64_t>(1, std::min<int64_t>(64, pl.nsamp / 1024));
   pl.nloss = loss_blocks_for(n);
