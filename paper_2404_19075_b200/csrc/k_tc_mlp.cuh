@@ -85,7 +85,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_mlp(TcParams p) {
   float *sB = sWo + H + 4;
   uint64_t *bars = reinterpret_cast<uint64_t *>(sB + C * 4);
   uint64_t *mma_bar = bars, *w_bar = bars + 2;  // mma_bar[cg]: N-half cg of the current MMA retired
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 3);
+  uint64_t *sa_ok = bars + 3;                    // MODE 1: sA may be rewritten (see the epilogue)
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 4);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (warp == 0) {
@@ -96,6 +97,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_mlp(TcParams p) {
     mbar_init(&mma_bar[0], 1);
     mbar_init(&mma_bar[1], 1);
     mbar_init(w_bar, 1);
+    mbar_init(sa_ok, 1);
     fence_mbar_init();
   }
   const int64_t per = (int64_t)H * H + H;
@@ -110,7 +112,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_mlp(TcParams p) {
   const uint32_t tmem_row = tmem + ((uint32_t)((warp & 3) * 32) << 16);
   const int cg = tid >> 7;                     // column half of this thread
   const int cb_lo = cg * (H / 64), cb_hi = (cg + 1) * (H / 64);  // its 32-column chunks
-  float *sMu = reinterpret_cast<float *>(bars + 4);  // [2][128] per-half head partials (forward)
+  float *sMu = reinterpret_cast<float *>(bars + 5);  // [2][128] per-half head partials (forward)
   const int n_tiles = (int)((p.nsamp + 127) / 128);
 
   // Weight schedule (thread 0): the layer whose image sits in sW, and a pending load.
@@ -136,7 +138,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_mlp(TcParams p) {
   };
   if (tid == 0 && (int)blockIdx.x < n_tiles && (MODE != 2 || L >= 2)) w_issue(MODE == 2 ? L - 1 : 0);
 
-  uint32_t mma_phase = 0;
+  uint32_t mma_phase = 0, sa_phase = 0;
   float head_acc[H / 32];
 #pragma unroll
   for (int i = 0; i < H / 32; ++i) head_acc[i] = 0.f;
@@ -153,7 +155,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_mlp(TcParams p) {
     const int64_t g = (int64_t)tile * 128 + row;
     const bool valid = g < p.nsamp;
     bool inside = false;
-    if (MODE != 0) {  // the previous tile's last bulk store must be done reading sA
+    if (MODE == 2) {  // the previous tile's last bulk store must be done reading sA
       if (tid == 0) bulk_wait_read_all();
       __syncthreads();
     }
@@ -178,10 +180,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_mlp(TcParams p) {
           rb3 = ra.x + jj * rbv.x;    // x
         }
 #pragma unroll 1
-        for (int c0 = cg * (C / 2); c0 < (cg + 1) * (C / 2); c0 += 8) {
-          uint32_t pc[4], ps[4];
+        for (int c0 = cg * (C / 2); c0 < (cg + 1) * (C / 2); c0 += 16) {
+          uint32_t pc[8], ps[8];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
+          for (int q = 0; q < 8; ++q) {
             float cs[2], sn[2];
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
@@ -193,8 +195,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_mlp(TcParams p) {
             pc[q] = pack_bf16x2(cs[0], cs[1]);
             ps[q] = pack_bf16x2(sn[0], sn[1]);
           }
-          st_shared_v4(a_base + sw128_offset(row, c0, 128), pc[0], pc[1], pc[2], pc[3]);
-          st_shared_v4(a_base + sw128_offset(row, C + c0, 128), ps[0], ps[1], ps[2], ps[3]);
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            st_shared_v4(a_base + sw128_offset(row, c0 + 8 * hh, 128), pc[4 * hh], pc[4 * hh + 1], pc[4 * hh + 2], pc[4 * hh + 3]);
+            st_shared_v4(a_base + sw128_offset(row, C + c0 + 8 * hh, 128), ps[4 * hh], ps[4 * hh + 1], ps[4 * hh + 2],
+                         ps[4 * hh + 3]);
+          }
         }
       }
       fence_proxy_async_smem();
@@ -225,20 +231,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_mlp(TcParams p) {
         mbar_wait(&mma_bar[cg], mma_phase);
         mma_phase ^= 1;
         tc_fence_after();
-        if (tid == 0) {
-          mbar_wait(&mma_bar[1], mma_phase ^ 1);  // both halves retired before sW may be refilled
-          // prefetch the next weight image (streaming mode) now that sW is free
-          if (!resident) {
-            const int nxt = (l + 1) % L;
-            const bool has_next = (l + 1 < L) || more_tiles;
-            if (has_next && nxt != w_cur) w_issue(nxt);
-          }
-          if (MODE == 1) bulk_wait_read_all();
-        }
-        if (MODE == 1) __syncthreads();
         const bool last = (l == L - 1);
-#pragma unroll 1
-        for (int cb = cb_lo; cb < cb_hi; ++cb) {
+        // this thread's half of the layer output, kept in registers until the other half's MMA
+        // (which reads all of sA) has retired: h_{l+1} overwrites sA in place
+        constexpr int NCB = H / 64;
+        uint32_t hk[NCB][16];
+#pragma unroll
+        for (int c = 0; c < NCB; ++c) {
+          const int cb = cb_lo + c;
           uint32_t v[32];
           tmem_ld32(tmem_row + cb * 32, v);
           tmem_wait_ld();
@@ -270,21 +270,40 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_mlp(TcParams p) {
           }
           if (!last) {
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              uint32_t w4[4];
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const int i0 = 8 * q + 2 * e;
-                w4[e] = pack_bf16x2(z[i0] * sg[i0], z[i0 + 1] * sg[i0 + 1]);  // swish(z) = z s
-              }
-              st_shared_v4(a_base + sw128_offset(row, cb * 32 + 8 * q, 128), w4[0], w4[1], w4[2], w4[3]);
-            }
+            for (int i = 0; i < 16; ++i) hk[c][i] = pack_bf16x2(z[2 * i] * sg[2 * i], z[2 * i + 1] * sg[2 * i + 1]);  // swish = z s
           } else {
 #pragma unroll
             for (int i = 0; i < 32; ++i) mu_acc += sWo[cb * 32 + i] * (z[i] * sg[i]);
           }
         }
-        if (!last) fence_proxy_async_smem();
+        if (MODE == 1) {
+          // sA is rewritten below: both MMA halves and the bulk stash store of this layer's input
+          // must be done reading it; thread 0 (which issued the store) publishes that on sa_ok
+          if (tid == 0) {
+            mbar_wait(&mma_bar[1], mma_phase ^ 1);
+            bulk_wait_read_all();
+            if (!last) mbar_arrive(sa_ok);
+          } else if (!last) {
+            mbar_wait(sa_ok, sa_phase);
+          }
+          if (!last) sa_phase ^= 1;
+        } else if (cg == 0 && (!last || tid == 0)) {
+          mbar_wait(&mma_bar[1], mma_phase ^ 1);  // both halves retired
+        }
+        if (tid == 0 && !resident) {  // prefetch the next weight image (streaming mode) now that sW is free
+          const int nxt = (l + 1) % L;
+          const bool has_next = (l + 1 < L) || more_tiles;
+          if (has_next && nxt != w_cur) w_issue(nxt);
+        }
+        if (!last) {
+#pragma unroll
+          for (int c = 0; c < NCB; ++c)
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              st_shared_v4(a_base + sw128_offset(row, (cb_lo + c) * 32 + 8 * q, 128), hk[c][4 * q], hk[c][4 * q + 1],
+                           hk[c][4 * q + 2], hk[c][4 * q + 3]);
+          fence_proxy_async_smem();
+        }
         tc_fence_before();
         __syncthreads();
         if (MODE == 1 && !last && tid == 0) {  // input of layer l+1 for the dW GEMM
