@@ -139,9 +139,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_mlp(TcParams p) {
   if (tid == 0 && (int)blockIdx.x < n_tiles && (MODE != 2 || L >= 2)) w_issue(MODE == 2 ? L - 1 : 0);
 
   uint32_t mma_phase = 0, sa_phase = 0;
-  float head_acc[H / 32];
+  constexpr int NCB = H / 64;  // 32-column chunks of this thread's column half
+  float head_acc[NCB];
 #pragma unroll
-  for (int i = 0; i < H / 32; ++i) head_acc[i] = 0.f;
+  for (int i = 0; i < NCB; ++i) head_acc[i] = 0.f;
   float bo_acc = 0.f;
   const uint64_t pol_z = policy_evict_first();  // z stash: written once, read once by the next kernel
   constexpr bool kSplit = H >= 128;  // N halves need whole 64-column blocks for the MN-major dX operand
@@ -234,7 +235,6 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_mlp(TcParams p) {
         const bool last = (l == L - 1);
         // this thread's half of the layer output, kept in registers until the other half's MMA
         // (which reads all of sA) has retired: h_{l+1} overwrites sA in place
-        constexpr int NCB = H / 64;
         uint32_t hk[NCB][16];
 #pragma unroll
         for (int c = 0; c < NCB; ++c) {
@@ -335,15 +335,19 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_mlp(TcParams p) {
         bulk_prefetch_l2(p.zstash + ((size_t)(L - 2) * p.n_tiles + tile) * kZTile, kZTile);
       {
         const uint8_t *zsrc = p.zstash + (((size_t)(L - 1) * p.n_tiles + tile) * (H / 16) * 128 + row) * 32;
-#pragma unroll 1
-        for (int cb = cb_lo; cb < cb_hi; ++cb) {
-          float z[32];
-          uint4 zq4[4];
+        uint4 zt[NCB][4];  // all of this thread's z chunks in flight at once
 #pragma unroll
-          for (int qq = 0; qq < 2; ++qq) ld_global_v8_hint(zsrc + (size_t)(cb * 2 + qq) * 128 * 32, zq4[2 * qq], zq4[2 * qq + 1], pol_z);
+        for (int c = 0; c < NCB; ++c)
+#pragma unroll
+          for (int qq = 0; qq < 2; ++qq)
+            ld_global_v8_hint(zsrc + (size_t)((cb_lo + c) * 2 + qq) * 128 * 32, zt[c][2 * qq], zt[c][2 * qq + 1], pol_z);
+#pragma unroll
+        for (int c = 0; c < NCB; ++c) {
+          const int cb = cb_lo + c;
+          float z[32];
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
-            const uint4 zq = zq4[q];
+            const uint4 zq = zt[c][q];
             const uint32_t zz[4] = {zq.x, zq.y, zq.z, zq.w};
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
@@ -365,7 +369,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_mlp(TcParams p) {
               x[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
             }
           }
-          head_acc[cb] += x[0];
+          head_acc[c] += x[0];
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             uint32_t w4[4];
@@ -395,6 +399,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_mlp(TcParams p) {
       }
       // dX chain
       for (int l = L - 1; l >= 1; --l) {
+        // swish'(z_{l-1}) of this thread's chunks: loads in flight while the dX MMA runs
+        uint4 zq[NCB][4];
+        {
+          const uint8_t *zsrc = p.zstash + (((size_t)(l - 1) * p.n_tiles + tile) * (H / 16) * 128 + row) * 32;
+#pragma unroll
+          for (int c = 0; c < NCB; ++c)
+#pragma unroll
+            for (int qq = 0; qq < 2; ++qq)
+              ld_global_v8_hint(zsrc + (size_t)((cb_lo + c) * 2 + qq) * 128 * 32, zq[c][2 * qq], zq[c][2 * qq + 1], pol_z);
+        }
         if (tid == 0) {
           uint32_t wl = w_ready(l);
           tc_fence_after();
@@ -428,18 +442,15 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_mlp(TcParams p) {
           bulk_wait_read_all();
         }
         __syncthreads();
-        const uint8_t *zsrc = p.zstash + (((size_t)(l - 1) * p.n_tiles + tile) * (H / 16) * 128 + row) * 32;
-#pragma unroll 1
-        for (int cb = cb_lo; cb < cb_hi; ++cb) {
+#pragma unroll
+        for (int c = 0; c < NCB; ++c) {
+          const int cb = cb_lo + c;
           uint32_t v[32];
           tmem_ld32(tmem_row + cb * 32, v);
-          uint4 zq[4];
-#pragma unroll
-          for (int qq = 0; qq < 2; ++qq) ld_global_v8_hint(zsrc + (size_t)(cb * 2 + qq) * 128 * 32, zq[2 * qq], zq[2 * qq + 1], pol_z);
           tmem_wait_ld();
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
-            const uint32_t zz[4] = {zq[q].x, zq[q].y, zq[q].z, zq[q].w};
+            const uint32_t zz[4] = {zq[c][q].x, zq[c][q].y, zq[c][q].z, zq[c][q].w};
             uint32_t w4[4];
 #pragma unroll
             for (int e = 0; e < 4; ++e) {  // delta = e swish'(z), swish' stashed as bf16 by the forward
@@ -466,8 +477,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_mlp(TcParams p) {
     if (tid == 0) bulk_wait_read_all();
     __syncthreads();
 #pragma unroll
-    for (int cb = 0; cb < H / 32; ++cb)
-      if (cb >= cb_lo && cb < cb_hi) red[warp * (H + 1) + cb * 32 + lane] = head_acc[cb];
+    for (int c = 0; c < NCB; ++c) red[warp * (H + 1) + (cb_lo + c) * 32 + lane] = head_acc[c];
     if (lane == 0) red[warp * (H + 1) + H] = bo_acc;  // (zero for column-half-1 warps)
     __syncthreads();
     for (int k = tid; k <= H; k += kTcThreads) {
