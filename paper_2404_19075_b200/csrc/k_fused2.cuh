@@ -503,46 +503,35 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
         if (lane == 0) sP[(s * 4 + (warp & 3)) * 2 + ch] = a;
       }
       named_sync(1, EPI);
-      if (tid < pix_per_group) {
-        const int64_t pix = gi * pix_per_group + tid;
-        if (pix < p.n_pix) {
-          float pv[8], wqv[8];
-          for (int ss = 0; ss < p.S; ++ss) {
-            const int ray_l = tid * p.S + ss;
-            wqv[ss] = sWq[ray_l];  // prefetched at the start of the group
-            float acc = 0.f;
-            for (int c = 0; c < chunks_per_ray; ++c) {  // M = mu0 (w_o . h_L + b_o) over the chunk's 32 samples
-              const int q = ray_l * chunks_per_ray + c;
-              acc += sP[2 * q] + sP[2 * q + 1] + 32.f * sWo[H];
-            }
-            pv[ss] = wqv[ss] > 0.f ? wqv[ss] * (p.mu0 * acc) : 0.f;
-          }
-          float fh, T = 1.f, m = 0.f;
-          if (p.combine == DINR_LINEAR) {
-            float acc = 0.f;
-            for (int ss = 0; ss < p.S; ++ss) acc += pv[ss];
-            fh = acc / (float)p.S;
-          } else {
-            m = pv[0];
-            for (int ss = 1; ss < p.S; ++ss) m = fminf(m, pv[ss]);
-            float acc = 0.f;
-            for (int ss = 0; ss < p.S; ++ss) acc += expf(-(pv[ss] - m));
-            T = acc / (float)p.S;
-            fh = m - logf(T);
-          }
-          if (p.fhat) p.fhat[pix] = fh;
-          const float res = sY[tid] - fh;
-          loss_acc += res * res;
-          const float gg = -2.f * res * p.inv_n;
-          for (int ss = 0; ss < p.S; ++ss) {
-            const float pi = p.combine == DINR_LINEAR ? 1.f / (float)p.S : expf(-(pv[ss] - m)) / ((float)p.S * T);
-            const float us = gg * pi * wqv[ss] * p.mu0;
-            for (int c = 0; c < chunks_per_ray; ++c) sU[(tid * p.S + ss) * chunks_per_ray + c] = us;
-          }
-        } else {
-          for (int ss = 0; ss < p.S; ++ss)
-            for (int c = 0; c < chunks_per_ray; ++c) sU[(tid * p.S + ss) * chunks_per_ray + c] = 0.f;
-        }
+      // a9-a11 on warp 0: lane q < 8 = ray chunk q of the group (32 samples).  S * N_s divides 256
+      // and both are powers of two, so a ray is an aligned group of cpr = N_s / 32 lanes and a pixel
+      // an aligned group of S * cpr lanes: ray sums, the Beer's-law min / sum and the pixel's
+      // upstream factors are xor-butterflies inside those groups.
+      if (warp == 0) {
+        const int q = lane & 7, cpr = chunks_per_ray, gl = cpr * p.S;
+        const int ray_l = q / cpr, pix_l = ray_l / p.S;
+        const int64_t pix = gi * pix_per_group + pix_l;
+        const bool live = lane < 8 && pix < p.n_pix;
+        float a = sP[2 * q] + sP[2 * q + 1] + 32.f * sWo[H];  // chunk sum of w_o . h_L + b_o
+        for (int o = 1; o < cpr; o <<= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+        const float wq = sWq[ray_l];  // prefetched at the start of the group
+        const float pv = wq > 0.f ? wq * (p.mu0 * a) : 0.f;
+        const bool beer = p.combine != DINR_LINEAR;
+        float m = pv;
+        if (beer)
+          for (int o = cpr; o < gl; o <<= 1) m = fminf(m, __shfl_xor_sync(0xffffffffu, m, o));
+        const float e = beer ? expf(-(pv - m)) : pv;
+        float sum = (q % cpr == 0) ? e : 0.f;  // one term per ray
+        for (int o = 1; o < gl; o <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        const float T = sum / (float)p.S;
+        const float fh = beer ? m - logf(T) : T;
+        const bool leader = live && (q % gl) == 0;
+        if (leader && p.fhat) p.fhat[pix] = fh;
+        const float res = sY[pix_l] - fh;
+        if (leader) loss_acc += res * res;
+        const float gg = -2.f * res * p.inv_n;
+        const float pi = beer ? e / ((float)p.S * T) : 1.f / (float)p.S;
+        if (lane < 8) sU[q] = live ? gg * pi * wq * p.mu0 : 0.f;
       }
       named_sync(1, EPI);
       // head gradients (warps 0 and 4 of warpgroup 0 own all H columns)
