@@ -411,7 +411,7 @@ dinr_status launch_fused(dinr_ctx *c, const Plan &pl, const float *y, cudaStream
   p.B = c->d_B;
   p.wpack_half = c->d_wpack_half;
   p.y = y;
-  p.fhat = pl.fhat;
+  p.fhat = nullptr;  // training needs only the loss and u: no per-pixel projection store on the join
   p.ring = pl.ring;
   p.dw01 = pl.dw01 ? 1 : 0;
   p.hstash = pl.hstash;

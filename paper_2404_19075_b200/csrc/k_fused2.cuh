@@ -512,25 +512,37 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
         const int ray_l = q / cpr, pix_l = ray_l / p.S;
         const int64_t pix = gi * pix_per_group + pix_l;
         const bool live = lane < 8 && pix < p.n_pix;
+        const float inv_s = 1.f / (float)p.S;  // S is a power of two: exact
         float a = sP[2 * q] + sP[2 * q + 1] + 32.f * sWo[H];  // chunk sum of w_o . h_L + b_o
-        for (int o = 1; o < cpr; o <<= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) {  // the three butterfly levels, each used inside its group only
+          const float t = __shfl_xor_sync(0xffffffffu, a, o);
+          if (o < cpr) a += t;
+        }
         const float wq = sWq[ray_l];  // prefetched at the start of the group
         const float pv = wq > 0.f ? wq * (p.mu0 * a) : 0.f;
         const bool beer = p.combine != DINR_LINEAR;
         float m = pv;
-        if (beer)
-          for (int o = cpr; o < gl; o <<= 1) m = fminf(m, __shfl_xor_sync(0xffffffffu, m, o));
-        const float e = beer ? expf(-(pv - m)) : pv;
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) {
+          const float t = __shfl_xor_sync(0xffffffffu, m, o);
+          if (o >= cpr && o < gl) m = fminf(m, t);
+        }
+        const float e = beer ? __expf(m - pv) : pv;
         float sum = (q % cpr == 0) ? e : 0.f;  // one term per ray
-        for (int o = 1; o < gl; o <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-        const float T = sum / (float)p.S;
-        const float fh = beer ? m - logf(T) : T;
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) {
+          const float t = __shfl_xor_sync(0xffffffffu, sum, o);
+          if (o < gl) sum += t;
+        }
+        const float T = sum * inv_s;
+        const float fh = beer ? m - __logf(T) : T;
         const bool leader = live && (q % gl) == 0;
         if (leader && p.fhat) p.fhat[pix] = fh;
         const float res = sY[pix_l] - fh;
         if (leader) loss_acc += res * res;
         const float gg = -2.f * res * p.inv_n;
-        const float pi = beer ? e / ((float)p.S * T) : 1.f / (float)p.S;
+        const float pi = beer ? __fdividef(e, sum) : inv_s;  // e^{-(p - m)} / (S T)
         if (lane < 8) sU[q] = live ? gg * pi * wq * p.mu0 : 0.f;
       }
       named_sync(1, EPI);
@@ -688,7 +700,9 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
       }
     }
     float *red = sHsum;  // reuse: [2 streams][4 row chunks][H + 4]
-    for (int j = 0; j < nf; ++j) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {  // static j: dbacc stays in registers
+      if (j >= nf) break;
       named_sync(1, EPI);
 #pragma unroll
       for (int c = 0; c < NCH; ++c) red[(s * 4 + (warp & 3)) * (H + 4) + ch * (H / 2) + c * 32 + lane] = dbacc[j][c];
