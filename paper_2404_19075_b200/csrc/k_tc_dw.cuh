@@ -31,6 +31,12 @@ struct DwParams {
   Jitter jit;
 };
 
+// The tensor core's fp32 accumulation loses precision with the length of the chain of MMAs into
+// one TMEM accumulator (measured: the cone512 gradient's deviation from batch linearity grew in
+// proportion to the tiles per CTA, 1.3e-3 at 2730 tiles).  Non-feature CTAs therefore restart the
+// accumulator every kDwFlushTiles tiles and warps 2-9 add it into fp32 registers.
+constexpr int kDwFlushTiles = 64;
+
 template <int H>
 struct DwLayout {
   static constexpr uint32_t A_STAGE = 32768;  // two 64-feature blocks (second is zero for H = 64)
@@ -54,7 +60,8 @@ __global__ void __launch_bounds__(DwLayout<H>::NT, 1) k_tc_dw(DwParams p) {
   uint64_t *full = reinterpret_cast<uint64_t *>(sB4 + H / 2);
   uint64_t *empty = full + NST;
   uint64_t *done = empty + NST;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(done + 1);
+  uint64_t *flush_full = done + 1, *flush_free = done + 2;  // accumulator chunk complete / read out
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(done + 3);
 
   const int tid = threadIdx.x, warp = tid >> 5;
   const int bx = blockIdx.x, mb = blockIdx.y;
@@ -62,6 +69,7 @@ __global__ void __launch_bounds__(DwLayout<H>::NT, 1) k_tc_dw(DwParams p) {
   const int split = bx < p.ks0 ? bx : (bx - p.ks0) % p.ks1;
   const int ks = l == 0 ? p.ks0 : p.ks1;
   const bool feat = p.feat0 && l == 0;
+  const bool fl = !feat;  // chunked accumulation (warps 2-9 are free to flush)
   if (warp == 0) {
     tmem_alloc(tmem_slot, LY::TMEM_COLS);
     tmem_relinquish();
@@ -72,6 +80,8 @@ __global__ void __launch_bounds__(DwLayout<H>::NT, 1) k_tc_dw(DwParams p) {
       mbar_init(&empty[s], 1);
     }
     mbar_init(done, 1);
+    mbar_init(flush_full, 1);
+    mbar_init(flush_free, 8);
     fence_mbar_init();
   }
   // constant operands: all-ones tile (bf16 1.0 = 0x3F80) and, for H = 64, zero pad blocks
@@ -112,7 +122,9 @@ __global__ void __launch_bounds__(DwLayout<H>::NT, 1) k_tc_dw(DwParams p) {
     const uint32_t ones_a = smem_u32(ones);
     for (int it = 0; it < count; ++it) {
       int st = it % NST;
+      const int ci = fl ? it % kDwFlushTiles : it;  // tile index within the accumulator chunk
       mbar_wait(&full[st], (it / NST) & 1);
+      if (fl && ci == 0 && it > 0) mbar_wait(flush_free, ((it / kDwFlushTiles) - 1) & 1);
       tc_fence_after();
       uint32_t sa = smem_u32(smem + st * LY::STAGE), sb = sa + LY::A_STAGE;
 #pragma unroll
@@ -120,11 +132,12 @@ __global__ void __launch_bounds__(DwLayout<H>::NT, 1) k_tc_dw(DwParams p) {
         uint64_t ad = sdesc_sw128(sa + kk * 2048, 16384, 1024);
         uint64_t bd = sdesc_sw128(sb + kk * 2048, 16384, 1024);
         uint64_t od = sdesc_sw128(ones_a + (kk & 3) * 32, 16, 1024);
-        uint32_t acc = (it > 0 || kk > 0) ? 1u : 0u;
+        uint32_t acc = (ci > 0 || kk > 0) ? 1u : 0u;
         umma_bf16(tmem_dw, ad, bd, id_dw, acc);
         umma_bf16(tmem_db, ad, od, id_db, acc);
       }
       umma_commit(&empty[st]);
+      if (fl && (ci == kDwFlushTiles - 1 || it == count - 1)) umma_commit(flush_full);
     }
     umma_commit(done);
   } else if (warp >= 2 && feat) {
@@ -152,13 +165,58 @@ __global__ void __launch_bounds__(DwLayout<H>::NT, 1) k_tc_dw(DwParams p) {
       if ((tid & 31) == 0) mbar_arrive(&full[st]);
     }
   }
+  if (fl && warp >= 2 && warp < 10) {
+    // flush warps: thread = (accumulator lane o, column half cp); every chunk of kDwFlushTiles
+    // tiles is added into fp32 registers, then the partial row is written from them
+    const int q4 = warp & 3, cp = (warp - 2) >> 2, o = (q4 << 5) | (tid & 31);
+    const uint32_t trow = (uint32_t)(q4 * 32) << 16;
+    float racc[H / 2], rdb = 0.f;
+#pragma unroll
+    for (int i = 0; i < H / 2; ++i) racc[i] = 0.f;
+    const int nch = (count + kDwFlushTiles - 1) / kDwFlushTiles;
+    for (int c = 0; c < nch; ++c) {
+      mbar_wait(flush_full, c & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int cb = 0; cb < H / 64; ++cb) {
+        uint32_t v[32];
+        tmem_ld32(tmem_dw + trow + cp * (H / 2) + cb * 32, v);
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) racc[cb * 32 + i] += __uint_as_float(v[i]);
+      }
+      if (cp == 0) {
+        uint32_t v[16];
+        tmem_ld16(tmem_db + trow, v);
+        tmem_wait_ld();
+        rdb += __uint_as_float(v[0]);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if ((tid & 31) == 0) mbar_arrive(flush_free);
+    }
+    const bool live = (H >= 128) || o < 64;
+    if (live) {
+      float *dst = p.dw_part + ((((size_t)l * p.nmb + mb) * p.ksplit + split) * 128 + o) * H + cp * (H / 2);
+#pragma unroll
+      for (int q = 0; q < H / 8; ++q)
+        reinterpret_cast<float4 *>(dst)[q] = make_float4(racc[4 * q], racc[4 * q + 1], racc[4 * q + 2], racc[4 * q + 3]);
+      if (cp == 0) p.db_part[(((size_t)l * p.nmb + mb) * p.ksplit + split) * 128 + o] = rdb;
+      // slots this layer does not use (ks < ksplit) are zero for the fixed-order reduction
+      for (int s2 = split + ks; s2 < p.ksplit; s2 += ks) {
+        float4 *z = reinterpret_cast<float4 *>(p.dw_part + ((((size_t)l * p.nmb + mb) * p.ksplit + s2) * 128 + o) * H + cp * (H / 2));
+        for (int q = 0; q < H / 8; ++q) z[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (cp == 0) p.db_part[(((size_t)l * p.nmb + mb) * p.ksplit + s2) * 128 + o] = 0.f;
+      }
+    }
+  }
   __syncwarp();
   if (count > 0) {
     mbar_wait(done, 0);
     tc_fence_after();
   }
-  // epilogue (warps 2-5): lane o of the accumulator -> fp32 partial row
-  if (warp >= 2 && warp < 6) {
+  // epilogue of feature CTAs (warps 2-5): lane o of the accumulator -> fp32 partial row
+  if (!fl && warp >= 2 && warp < 6) {
     const int o = ((warp & 3) << 5) | (tid & 31);
     const uint32_t trow = (uint32_t)((warp & 3) * 32) << 16;
     float *dst = p.dw_part + ((((size_t)l * p.nmb + mb) * p.ksplit + split) * 128 + o) * H;

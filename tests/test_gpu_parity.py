@@ -231,6 +231,37 @@ def test_full_size_batch_sampled(ctx, dev, O, name):
     assert np.all(np.isfinite(fhat.cpu().numpy()))
 
 
+@pytest.mark.parametrize("name", ["fan512", "cone512"])
+def test_full_size_gradient_is_batch_linear(ctx, dev, name):
+    """The training step at the BASELINE batch, in the bench launch configuration (every CTA busy,
+    full K-splits, the fused path's ring and stashes at full size), against the same step run as
+    four quarter batches: the loss and the gradient are means over pixels, so the full-batch values
+    must be the means of the quarters.  Exact quarters scale the upstream factors (and so every
+    bf16-rounded delta) by exactly 4, so per-sample arithmetic is identical up to that power of two
+    and only the fp32 reduction order differs (tolerance 1e-4 of the largest entry per tensor;
+    uneven splits would re-round every delta in bf16: ~1e-3 after the pixel sum's cancellation)."""
+    g, th, t, f, B, prm = setup_case(ctx, dev, name, {}, {}, "bf16", "beer")
+    n = synth.WORKLOADS[name]["batch"]
+    idx = torch.tensor(synth.pixel_batch(name, n, seed=5), device=dev)
+    y = torch.tensor(synth.synthetic_y(n, 1.0, seed=6), device=dev)
+    P = synth.param_count(f["C"], f["L"])
+    full = torch.zeros(P + 1, device=dev)
+    D.project_and_grad(ctx, idx, y, full)
+    acc = torch.zeros(P + 1, dtype=torch.float64, device=dev)
+    assert n % 4 == 0
+    for k in range(4):
+        a, b = k * n // 4, (k + 1) * n // 4
+        part = torch.zeros(P + 1, device=dev)
+        D.project_and_grad(ctx, idx[a:b].contiguous(), y[a:b].contiguous(), part)
+        acc += part.double() * 0.25
+    torch.cuda.synchronize()
+    full, acc = full.double().cpu().numpy(), acc.cpu().numpy()
+    assert np.all(np.isfinite(full))
+    assert abs(full[P] - acc[P]) <= 1e-4 * abs(acc[P])  # loss
+    errs = tensor_errs(full[:P], acc[:P], f["C"], f["L"])
+    assert max(errs) <= 1e-4, errs
+
+
 def test_adam_step_parity_and_repack(ctx, dev, O):
     """N1: the fused Adam + re-pack kernel matches the oracle's Adam (fp32 tolerance) and the
     re-packed bf16 images equal those of dinr_set_field_weights on the updated parameters."""
