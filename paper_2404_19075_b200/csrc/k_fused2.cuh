@@ -508,11 +508,13 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
       // an aligned group of S * cpr lanes: ray sums, the Beer's-law min / sum and the pixel's
       // upstream factors are xor-butterflies inside those groups.
       if (warp == 0) {
-        const int q = lane & 7, cpr = chunks_per_ray, gl = cpr * p.S;
-        const int ray_l = q / cpr, pix_l = ray_l / p.S;
+        // powers of two throughout: shifts and masks, no integer or fp32 divisions on the join
+        const int lg_cpr = p.lg_ns - 5, lg_s = __ffs(p.S) - 1;
+        const int q = lane & 7, cpr = 1 << lg_cpr, gl = cpr << lg_s;
+        const int ray_l = q >> lg_cpr, pix_l = ray_l >> lg_s;
         const int64_t pix = gi * pix_per_group + pix_l;
         const bool live = lane < 8 && pix < p.n_pix;
-        const float inv_s = 1.f / (float)p.S;  // S is a power of two: exact
+        const float inv_s = __int_as_float((127 - lg_s) << 23);  // 1 / S exactly
         float a = sP[2 * q] + sP[2 * q + 1] + 32.f * sWo[H];  // chunk sum of w_o . h_L + b_o
 #pragma unroll
         for (int o = 1; o < 8; o <<= 1) {  // the three butterfly levels, each used inside its group only
@@ -529,7 +531,7 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
           if (o >= cpr && o < gl) m = fminf(m, t);
         }
         const float e = beer ? __expf(m - pv) : pv;
-        float sum = (q % cpr == 0) ? e : 0.f;  // one term per ray
+        float sum = (q & (cpr - 1)) == 0 ? e : 0.f;  // one term per ray
 #pragma unroll
         for (int o = 1; o < 8; o <<= 1) {
           const float t = __shfl_xor_sync(0xffffffffu, sum, o);
@@ -537,7 +539,7 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
         }
         const float T = sum * inv_s;
         const float fh = beer ? m - __logf(T) : T;
-        const bool leader = live && (q % gl) == 0;
+        const bool leader = live && (q & (gl - 1)) == 0;
         if (leader && p.fhat) p.fhat[pix] = fh;
         const float res = sY[pix_l] - fh;
         if (leader) loss_acc += res * res;
