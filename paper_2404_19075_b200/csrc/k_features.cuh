@@ -86,7 +86,18 @@ struct VoxGrid {
 // Normalized (t, z, y, x) of voxel v (fp64 centre, rounded once to fp32) and whether the centre
 // lies in the FOV cylinder (x - x_s0)^2 + y^2 <= r^2, decided in fp64 without contraction.
 __device__ __forceinline__ float4 voxel_coords(const VoxGrid &vg, int64_t v, bool &inside) {
-  const int64_t i = v % vg.nx, j = (v / vg.nx) % vg.ny, k = vg.k0 + v / (vg.nx * vg.ny);
+  int64_t i, j, k;
+  if ((v >> 32) == 0 && (vg.nx >> 16) == 0 && (vg.ny >> 16) == 0) {  // 32-bit divisions (the 64-bit ones are calls)
+    const uint32_t v32 = (uint32_t)v, nx = (uint32_t)vg.nx, ny = (uint32_t)vg.ny;
+    const uint32_t r = v32 / nx;
+    i = v32 - r * nx;
+    j = r % ny;
+    k = vg.k0 + r / ny;
+  } else {
+    i = v % vg.nx;
+    j = (v / vg.nx) % vg.ny;
+    k = vg.k0 + v / (vg.nx * vg.ny);
+  }
   const double x = dadd(vg.x0, dmul(dadd((double)i, 0.5), vg.vx));
   const double y = dadd(vg.y0, dmul(dadd((double)j, 0.5), vg.vy));
   const double z = dadd(vg.z0, dmul(dadd((double)k, 0.5), vg.vz));

@@ -54,6 +54,12 @@ struct TcLayout {
   }
 };
 
+// ray of sample g: 32-bit division whenever g fits (every training batch; the 64-bit division is
+// a long subroutine call)
+__device__ __forceinline__ int64_t ray_of(int64_t g, int n_s) {
+  return (g >> 32) == 0 ? (int64_t)((uint32_t)g / (uint32_t)n_s) : g / n_s;
+}
+
 __device__ __forceinline__ float swish_f(float z) { return z * (0.5f + 0.5f * tanh_approx(0.5f * z)); }
 __device__ __forceinline__ float dswish_f(float z) {
   float s = 0.5f + 0.5f * tanh_approx(0.5f * z);
@@ -171,7 +177,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_mlp(TcParams p) {
           rb2 = r.z;
           rb3 = r.w;
         } else if (valid) {
-          int64_t ray = g / p.n_s;
+          int64_t ray = ray_of(g, p.n_s);
           const uint32_t jr = (uint32_t)(g - ray * p.n_s);
           float jj = (float)jr + sample_offset(p.jit, ray, jr);
           float4 ra = p.rec32[2 * ray], rbv = p.rec32[2 * ray + 1];
@@ -329,7 +335,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_mlp(TcParams p) {
       // ---------------------------------------------------------------- a12 backward (MODE 2)
       // top layer from the stashed z_{L-1}: h_L = swish(z) for the head gradients (transpose-
       // reduce u h_L over the warp's 32 rows), delta_L = u w_o swish'(z)
-      const float u_row = valid ? p.u[g / p.n_s] : 0.f;
+      const float u_row = valid ? p.u[ray_of(g, p.n_s)] : 0.f;
       constexpr uint32_t kZTile = 128u * H * 2u;  // one tile of fp16 z
       if (tid == 0 && L >= 2)  // z_{L-2} is read after the first dX: bring it to L2 now
         bulk_prefetch_l2(p.zstash + ((size_t)(L - 2) * p.n_tiles + tile) * kZTile, kZTile);
