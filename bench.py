@@ -393,6 +393,16 @@ def main():
             roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                     "traffic": profiled_traffic(name, dom, path_kind), "kernel": dom, "peak_source": f"{peak_src} HBM copy"}
         step_tflops = value * fps / 1e12
+        # configs with small H can be bound by the MUFU (tanh per activation, sin/cos per
+        # frequency: L*H + 2C per sample forward) or the FP32/FMA pipe (~10 epilogue ops per
+        # activation fwd+bwd) rather than the tensor core.  Unit rates per SM per clock: MUFU 16,
+        # FMA 128; clocks.max.sm 1965 MHz, 148 SMs (B200_PROFILING.md) -- DESIGN.md "Binding roofline".
+        sm_rate = 148 * 1.965e9 * world
+        C = H // 2
+        rates = {"tensor": tf_burst * 1e12 * world / fps, "mufu": 16 * sm_rate / (L * H + 2 * C),
+                 "fma": 128 * sm_rate / (10.0 * L * H)}
+        bind = min(rates, key=rates.get)
+        binding = {"bound": bind, "samples_per_s": {k: v for k, v in rates.items()}, "frac": value / rates[bind]}
         base_rate, base_px, base_dt = (None, 0, 0.0)
         if args.cpu_baseline_seconds > 0 and world == 1:
             base_rate, base_px, base_dt = oracle_rate(name, budget_s=args.cpu_baseline_seconds)
@@ -409,6 +419,7 @@ def main():
             "step_roofline": {"flop_per_sample": fps, "achieved_tflops": step_tflops,
                               "frac_burst": step_tflops / tf_burst,
                               "frac_sustained": step_tflops / tf_sust if tf_sust else None},
+            "binding_roofline": binding,
             "kernel_ms_per_step": {k: v[0] / args.steps for k, v in ktimes.items()},
             "cpu_baseline": ({"value": base_rate, "unit": UNIT, "cores": cores(), "kind": "oracle",
                               "sample": f"{base_px} pixels ({base_px * S * ns} samples) of {name}, "
