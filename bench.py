@@ -375,8 +375,8 @@ def main():
             "forward": ("tensor", 2.0 * L * H * H * nsamp),
             "backward": ("tensor", 2.0 * ((L + (L - 1) + nf) if fused else (L - 1)) * H * H * nsamp),
             "dw": ("tensor", 2.0 * (L - nf) * H * H * nsamp),
-            "rays": ("hbm", n * (8 + S * 32.0)),
-            "loss": ("hbm", n * (4 + 4 + S * (32 + 4.0 * (ns // 32)) + S * 4)),
+            "rays": ("hbm", n * (8 + S * 36.0)),
+            "loss": ("hbm", n * (4 + 4 + S * (4 + 4.0 * (ns // 32)) + S * 4)),
         }
         shares = {k: v[0] for k, v in ktimes.items()}
         dom = max((k for k in alg), key=lambda k: shares.get(k, 0.0))

@@ -113,6 +113,7 @@ struct Plan {
   uint2 *rid;   // global ray ids (N3 keys)
   Jitter jit;   // N3 sample placement handed to the MLP kernels
   float *pchunk, *u, *fhat, *loss_part, *head_part, *dw_part, *db_part, *colsum;
+  float *wq;  // per-ray quadrature weight (K1 -> K4)
   uint8_t *hstash, *dstash, *zstash;
   float *sh, *sz, *sd;
   int64_t *idx_dev;
@@ -164,6 +165,7 @@ size_t plan_layout(dinr_ctx *c, int64_t n, bool train, bool host_io, Plan &pl, v
   pl.jit.step = c->step;
   pl.pchunk = ar.take<float>(pl.nsamp / kChunk + 1);
   pl.u = ar.take<float>(pl.n_rays + 1);
+  pl.wq = ar.take<float>(pl.n_rays + 1);
   pl.fhat = ar.take<float>(n + 1);
   pl.loss_part = ar.take<float>(pl.nloss + 1);
   const bool simt = c->field.precision == DINR_FP32_VERIFY;
@@ -297,12 +299,12 @@ dinr_status set_smem(dinr_ctx *c, K kernel, size_t bytes) {
 }
 
 dinr_status launch_rays(dinr_ctx *c, const int64_t *idx, int64_t n, double *rec64, float4 *rec32, uint2 *rid,
-                        cudaStream_t st) {
+                        cudaStream_t st, float *wq = nullptr) {
   if (n == 0) return DINR_OK;
   int64_t threads = n * c->S;
   Launch L_(c, T_RAYS, st);
   k_ray_setup<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(geom_params(c), c->d_views, idx, n, rec64, rec32,
-                                                                  rid, c->d_flags);
+                                                                  rid, c->d_flags, wq);
   CUDA_TRY(c, cudaGetLastError());
   return DINR_OK;
 }
@@ -641,7 +643,7 @@ dinr_status run_loss(dinr_ctx *c, const Plan &pl, const float *y, float *fhat, f
                      float *Ihat, cudaStream_t st) {
   if (pl.n == 0) return DINR_OK;
   Launch L_(c, T_LOSS, st);
-  k_loss<<<pl.nloss, kLossThreads, 0, st>>>(pl.rec32, pl.pchunk, c->S, pl.nc, pl.n, y, c->field.combine,
+  k_loss<<<pl.nloss, kLossThreads, 0, st>>>(pl.wq, pl.pchunk, c->S, pl.nc, pl.n, y, c->field.combine,
                                             (float)c->field.mu0, fhat, p_sub, I0, Ihat, pl.u,
                                             y ? pl.loss_part : nullptr);
   CUDA_TRY(c, cudaGetLastError());
@@ -655,7 +657,7 @@ dinr_status step_grad(dinr_ctx *c, const int64_t *idx, int64_t n, const float *y
     if (!accumulate) CUDA_TRY(c, cudaMemsetAsync(grad, 0, sizeof(float) * (c->P + 1), st));
     return DINR_OK;
   }
-  s = launch_rays(c, idx, n, nullptr, pl.rec32, pl.jit.rid ? pl.rid : nullptr, st);
+  s = launch_rays(c, idx, n, nullptr, pl.rec32, pl.jit.rid ? pl.rid : nullptr, st, pl.wq);
   if (s) return s;
   if (pl.fused) {
     s = c->H == 64 ? launch_fused<64>(c, pl, y, st) : launch_fused<128>(c, pl, y, st);
@@ -975,7 +977,7 @@ dinr_status dinr_project(dinr_ctx *c, const int64_t *idx, int64_t n, float *fhat
   Plan pl;
   dinr_status s = ensure_plan(c, n, false, false, pl);
   if (s) return s;
-  s = launch_rays(c, idx, n, nullptr, pl.rec32, pl.jit.rid ? pl.rid : nullptr, st);
+  s = launch_rays(c, idx, n, nullptr, pl.rec32, pl.jit.rid ? pl.rid : nullptr, st, pl.wq);
   if (s) return s;
   s = c->field.precision == DINR_FP32_VERIFY ? simt_forward(c, pl, st) : tc_forward(c, pl, 0, st);
   if (s) return s;

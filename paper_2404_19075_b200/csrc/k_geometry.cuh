@@ -99,7 +99,7 @@ __device__ __forceinline__ bool ray_fp64(const GeomParams &gp, const double *__r
 
 __global__ void k_ray_setup(GeomParams gp, const double *__restrict__ views, const int64_t *__restrict__ idx,
                             int64_t n, double *__restrict__ rec64, float4 *__restrict__ rec32,
-                            uint2 *__restrict__ rid, int *__restrict__ flags) {
+                            uint2 *__restrict__ rid, int *__restrict__ flags, float *__restrict__ wq) {
   const int S = gp.sub_x * gp.sub_z;
   int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (gid >= n * S) return;
@@ -118,6 +118,7 @@ __global__ void k_ray_setup(GeomParams gp, const double *__restrict__ views, con
       rec32[2 * gid] = make_float4(0.f, 0.f, 0.f, 0.f);
       rec32[2 * gid + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
+    if (wq) wq[gid] = 0.f;
     return;
   }
   const double ox = rr[0], oy = rr[1], oz = rr[2], dx = rr[3], dy = rr[4], dz = rr[5];
@@ -133,8 +134,9 @@ __global__ void k_ray_setup(GeomParams gp, const double *__restrict__ views, con
     float tb = gp.th > 0.0 ? (float)((tk - gp.tc) / gp.th) : 0.f;
     bool hit = chord > 0.0;
     rec32[2 * gid] = make_float4((float)((ex0 - gp.xs0) * ir), (float)(ey0 * ir), (float)((ez0 - gp.zc) * izh), tb);
-    rec32[2 * gid + 1] = make_float4((float)(step * dx * ir), (float)(step * dy * ir), (float)(step * dz * izh),
-                                     hit ? (float)(chord / (double)gp.n_s) : 0.f);
+    const float w = hit ? (float)(chord / (double)gp.n_s) : 0.f;
+    rec32[2 * gid + 1] = make_float4((float)(step * dx * ir), (float)(step * dy * ir), (float)(step * dz * izh), w);
+    if (wq) wq[gid] = w;  // compact copy for the pixel combine (one 4-byte read per ray)
   }
 }
 

@@ -40,7 +40,7 @@ __global__ void k_pack_weights(const float *__restrict__ params, int H, int L, u
 constexpr int kLossThreads = 256;
 constexpr int kMaxS = 16;
 
-__global__ void __launch_bounds__(kLossThreads) k_loss(const float4 *__restrict__ rec32, const float *__restrict__ pchunk,
+__global__ void __launch_bounds__(kLossThreads) k_loss(const float *__restrict__ wqa, const float *__restrict__ pchunk,
                                                        int S, int nc, int64_t n, const float *__restrict__ y,
                                                        int combine, float mu0, float *__restrict__ fhat,
                                                        float *__restrict__ p_sub, const float *__restrict__ I0,
@@ -52,7 +52,7 @@ __global__ void __launch_bounds__(kLossThreads) k_loss(const float4 *__restrict_
     float p[kMaxS], wq[kMaxS];
     for (int s = 0; s < S; ++s) {
       int64_t ray = i * S + s;
-      wq[s] = rec32[2 * ray + 1].w;
+      wq[s] = wqa[ray];  // quadrature weight chord / N_s (K1's compact copy)
       float acc = 0.f;
       for (int c = 0; c < nc; ++c) acc += pchunk[ray * nc + c];
       p[s] = wq[s] > 0.f ? wq[s] * acc : 0.f;
