@@ -289,6 +289,11 @@ GeomParams geom_params(const dinr_ctx *c) {
   gp.seed_lo = (uint32_t)c->seed;
   gp.seed_hi = (uint32_t)(c->seed >> 32);
   gp.step = c->step;
+  gp.ir = 1.0 / gp.r;
+  gp.izh = gp.zh > 0.0 ? 1.0 / gp.zh : 0.0;
+  gp.inv_sub_x = 1.0 / (double)gp.sub_x;
+  gp.inv_sub_z = 1.0 / (double)gp.sub_z;
+  gp.inv_ns = 1.0 / (double)gp.n_s;
   return gp;
 }
 

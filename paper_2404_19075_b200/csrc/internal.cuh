@@ -26,6 +26,9 @@ struct GeomParams {
   int64_t M;              // number of views
   int jitter;             // N3: sub-pixel jitter on (seed, step below)
   uint32_t seed_lo, seed_hi, step;
+  // host-computed reciprocals (correctly rounded, so identical to the device division):
+  // inv_sub_* is used only when sub_* is a power of two (then x * (1/sub) == x / sub exactly)
+  double ir, izh, inv_sub_x, inv_sub_z, inv_ns;  // inv_ns likewise only for N_s a power of two
 };
 
 // Per-ray packed fp32 record (2 x float4), produced by K1, consumed by the MLP kernels:

@@ -38,8 +38,19 @@ __device__ __forceinline__ bool ray_fp64(const GeomParams &gp, const double *__r
   int u = s % gp.sub_x, v = s / gp.sub_x;
   int64_t N = (int64_t)gp.n_rows * gp.n_cols;
   if (i < 0 || i >= gp.M * N) return false;
-  int64_t k = i / N, nn = i % N;
-  int64_t row = nn / gp.n_cols, col = nn % gp.n_cols;
+  int64_t k, row, col;
+  if ((i >> 32) == 0 && (N >> 32) == 0) {  // 32-bit divisions (the 64-bit ones are subroutine calls)
+    const uint32_t i32 = (uint32_t)i, N32 = (uint32_t)N, nc = (uint32_t)gp.n_cols;
+    const uint32_t k32 = i32 / N32, nn = i32 - k32 * N32, r32 = nn / nc;
+    k = k32;
+    row = r32;
+    col = nn - r32 * nc;
+  } else {
+    const int64_t nn = i % N;
+    k = i / N;
+    row = nn / gp.n_cols;
+    col = nn % gp.n_cols;
+  }
   double ck = views[3 * k], sk = views[3 * k + 1];
   tk = views[3 * k + 2];
 
@@ -52,9 +63,14 @@ __device__ __forceinline__ bool ray_fp64(const GeomParams &gp, const double *__r
     ux = (double)u01f(o.x);
     uz = (double)u01f(o.y);
   }
-  double xd = dadd(-gp.cx, dmul(dadd((double)col, __ddiv_rn(dadd((double)u, ux), (double)gp.sub_x)), gp.dx));
+  // (u + ux) / D_x: a multiply by the exact reciprocal when D_x is a power of two (same result)
+  const double fx = (gp.sub_x & (gp.sub_x - 1)) == 0 ? dmul(dadd((double)u, ux), gp.inv_sub_x)
+                                                     : __ddiv_rn(dadd((double)u, ux), (double)gp.sub_x);
+  const double fz = (gp.sub_z & (gp.sub_z - 1)) == 0 ? dmul(dadd((double)v, uz), gp.inv_sub_z)
+                                                     : __ddiv_rn(dadd((double)v, uz), (double)gp.sub_z);
+  double xd = dadd(-gp.cx, dmul(dadd((double)col, fx), gp.dx));
   double yd = gp.odd;
-  double zd = dadd(-gp.cz, dmul(dadd((double)row, __ddiv_rn(dadd((double)v, uz), (double)gp.sub_z)), gp.dz));
+  double zd = dadd(-gp.cz, dmul(dadd((double)row, fz), gp.dz));
   double xs, ys = -gp.sod, zs;
   if (gp.beam == DINR_CONE) {
     xs = 0.0;
@@ -103,7 +119,7 @@ __global__ void k_ray_setup(GeomParams gp, const double *__restrict__ views, con
   const int S = gp.sub_x * gp.sub_z;
   int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (gid >= n * S) return;
-  int64_t p = gid / S;
+  const int64_t p = (gid >> 32) == 0 ? (int64_t)((uint32_t)gid / (uint32_t)S) : gid / S;
   int s = (int)(gid - p * S);
   double rr[9], tk;
   if (rid) {  // global ray id, keys the N3 sample offsets in the MLP kernels
@@ -127,14 +143,14 @@ __global__ void k_ray_setup(GeomParams gp, const double *__restrict__ views, con
     for (int q = 0; q < 9; ++q) rec64[gid * 9 + q] = rr[q];
   if (rec32) {
     // Normalized entry point and per-sample step (R11); weight chord/N_s (R7).
-    double ir = 1.0 / gp.r;
-    double izh = gp.zh > 0.0 ? 1.0 / gp.zh : 0.0;
+    const double ir = gp.ir, izh = gp.izh;  // host-computed 1/r, 1/z_h (same rounding as here)
     double ex0 = ox + dmin * dx, ey0 = oy + dmin * dy, ez0 = oz + dmin * dz;
-    double step = (dmax - dmin) / (double)gp.n_s;
+    const bool ns_pow2 = (gp.n_s & (gp.n_s - 1)) == 0;  // then x / N_s == x * (1 / N_s) exactly
+    double step = ns_pow2 ? (dmax - dmin) * gp.inv_ns : (dmax - dmin) / (double)gp.n_s;
     float tb = gp.th > 0.0 ? (float)((tk - gp.tc) / gp.th) : 0.f;
     bool hit = chord > 0.0;
     rec32[2 * gid] = make_float4((float)((ex0 - gp.xs0) * ir), (float)(ey0 * ir), (float)((ez0 - gp.zc) * izh), tb);
-    const float w = hit ? (float)(chord / (double)gp.n_s) : 0.f;
+    const float w = hit ? (float)(ns_pow2 ? chord * gp.inv_ns : chord / (double)gp.n_s) : 0.f;
     rec32[2 * gid + 1] = make_float4((float)(step * dx * ir), (float)(step * dy * ir), (float)(step * dz * izh), w);
     if (wq) wq[gid] = w;  // compact copy for the pixel combine (one 4-byte read per ray)
   }
