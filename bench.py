@@ -175,8 +175,8 @@ def run_reference(args, rank, world):
     B = synth.grff_matrix(f["C"], f["sigma_t"], f["sigma_s"])
     prm = synth.init_params(f["C"], f["L"])
     # bounded per-step sample, sized so W + K steps finish in about a minute
-    rate, _, _ = oracle_rate(name, budget_s=6.0)
-    per_step_samples = max(S * ns, int(rate * 50.0 / max(1, args.steps + args.warmup)))
+    rate, _, _ = oracle_rate(name, budget_s=min(6.0, args.ref_seconds / 4))
+    per_step_samples = max(S * ns, int(rate * args.ref_seconds / max(1, args.steps + args.warmup)))
     n = max(1, per_step_samples // (S * ns))
     times = []
     for it in range(args.warmup + args.steps):
@@ -211,6 +211,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--batch", type=int, default=0, help="pixels per GPU per step (default: workload's)")
     ap.add_argument("--cpu-baseline-seconds", type=float, default=15.0)
+    ap.add_argument("--ref-seconds", type=float, default=50.0,
+                    help="--impl reference: host time budget of the W + K oracle steps")
     ap.add_argument("--combine", default="beer", choices=["beer", "linear"])
     ap.add_argument("--strong", action="store_true",
                     help="strong scaling: the workload's batch is the global batch, split over the ranks")
