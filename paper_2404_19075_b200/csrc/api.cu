@@ -23,6 +23,7 @@
 #include "k_fused.cuh"
 #include "k_fused2.cuh"
 #include "k_dw01.cuh"
+#include "k_tc_fwd2.cuh"
 #include "k_infer.cuh"
 #include "k_phantom.cuh"
 #include "nccl_dl.cuh"
@@ -227,6 +228,9 @@ size_t plan_layout(dinr_ctx *c, int64_t n, bool train, bool host_io, Plan &pl, v
       pl.db_part = ar.take<float>((size_t)pl.nu * pl.ksplit * 128);
     }
   } else if (!simt && train) {
+    // the split path's training forward runs tiles in pairs (k_tc_fwd2): an even tile count; the
+    // padding tile holds only invalid samples, whose upstream factor and so delta are exactly zero
+    pl.n_tiles = 2 * ((pl.nsamp + 255) / 256);
     pl.hstash = ar.take<uint8_t>((size_t)L * pl.n_tiles * H * 256);
     pl.dstash = ar.take<uint8_t>((size_t)L * pl.n_tiles * H * 256);
     pl.zstash = ar.take<uint8_t>((size_t)L * pl.n_tiles * H * 256);
@@ -353,6 +357,14 @@ dinr_status launch_tc_mlp(dinr_ctx *c, const Plan &pl, int mode, cudaStream_t st
     if (s) return s;
     Launch L_(c, T_BWD, st);
     k_tc_mlp<H, 2><<<pl.grid_tc, kTcThreads, smem, st>>>(p);
+  } else if (mode == 1 && H == 256 && !std::getenv("DINR_NO_FWD2")) {
+    // two tile streams per CTA, W_l streamed in N-halves (k_tc_fwd2.cuh)
+    const size_t sm2 = Fwd2Layout::smem_bytes(c->L);
+    dinr_status s = set_smem(c, k_tc_fwd2, sm2);
+    if (s) return s;
+    Launch L_(c, T_FWD, st);
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(pl.n_tiles / 2, c->sm_count));
+    k_tc_fwd2<<<grid, Fwd2Layout::NT, sm2, st>>>(p);
   } else if (mode == 1) {
     dinr_status s = set_smem(c, k_tc_mlp<H, 1>, smem);
     if (s) return s;

@@ -119,7 +119,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_mlp(TcParams p) {
   const int cg = tid >> 7;                     // column half of this thread
   const int cb_lo = cg * (H / 64), cb_hi = (cg + 1) * (H / 64);  // its 32-column chunks
   float *sMu = reinterpret_cast<float *>(bars + 5);  // [2][128] per-half head partials (forward)
-  const int n_tiles = (int)((p.nsamp + 127) / 128);
+  // the training plan may round the tile count up (paired tiles): padding tiles hold invalid samples
+  const int n_tiles = (int)(p.n_tiles > (p.nsamp + 127) / 128 ? p.n_tiles : (p.nsamp + 127) / 128);
 
   // Weight schedule (thread 0): the layer whose image sits in sW, and a pending load.
   int w_cur = -1;
