@@ -348,6 +348,9 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
     const int rays_per_group = 256 / p.n_s;
     const int pix_per_group = rays_per_group / p.S;
     const int chunks_per_ray = p.n_s / 32;
+    // every tile holds whole pixels (S N_s <= 128): each stream combines its own pixels, no join.
+    // Compiled in for H = 64 only (parallel64: -2.7 %); at H = 128 the extra code cost fan512 +1.9 %
+    const bool sl = H == 64 && (128 % (p.S * p.n_s)) == 0;
 
     for (int64_t gi = blockIdx.x; gi < n_groups; gi += gridDim.x) {
       const int64_t tile = 2 * gi + s;
@@ -502,18 +505,24 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
         for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
         if (lane == 0) sP[(s * 4 + (warp & 3)) * 2 + ch] = a;
       }
-      named_sync(1, EPI);
+      if (sl)
+        asm volatile("bar.sync %0, 256;" ::"r"(2 + s) : "memory");
+      else
+        named_sync(1, EPI);
       // a9-a11 on warp 0: lane q < 8 = ray chunk q of the group (32 samples).  S * N_s divides 256
       // and both are powers of two, so a ray is an aligned group of cpr = N_s / 32 lanes and a pixel
       // an aligned group of S * cpr lanes: ray sums, the Beer's-law min / sum and the pixel's
       // upstream factors are xor-butterflies inside those groups.
-      if (warp == 0) {
+      // (sl: the first warp of each stream does its own tile's chunks 4s..4s+3 on lanes 0-3; pixels
+      // then span <= 4 chunks, so only the butterfly levels 1, 2 act)
+      if (sl ? (warp & 7) == 0 : warp == 0) {
         // powers of two throughout: shifts and masks, no integer or fp32 divisions on the join
         const int lg_cpr = p.lg_ns - 5, lg_s = __ffs(p.S) - 1;
-        const int q = lane & 7, cpr = 1 << lg_cpr, gl = cpr << lg_s;
+        const int nq = sl ? 4 : 8;
+        const int q = sl ? 4 * s + (lane & 3) : (lane & 7), cpr = 1 << lg_cpr, gl = cpr << lg_s;
         const int ray_l = q >> lg_cpr, pix_l = ray_l >> lg_s;
         const int64_t pix = gi * pix_per_group + pix_l;
-        const bool live = lane < 8 && pix < p.n_pix;
+        const bool live = lane < nq && pix < p.n_pix;
         const float inv_s = __int_as_float((127 - lg_s) << 23);  // 1 / S exactly
         float a = sP[2 * q] + sP[2 * q + 1] + 32.f * sWo[H];  // chunk sum of w_o . h_L + b_o
 #pragma unroll
@@ -545,23 +554,28 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
         if (leader) loss_acc += res * res;
         const float gg = -2.f * res * p.inv_n;
         const float pi = beer ? __fdividef(e, sum) : inv_s;  // e^{-(p - m)} / (S T)
-        if (lane < 8) sU[q] = live ? gg * pi * wq * p.mu0 : 0.f;
+        if (lane < nq) sU[q] = live ? gg * pi * wq * p.mu0 : 0.f;
       }
-      named_sync(1, EPI);
-      // head gradients (warps 0 and 4 of warpgroup 0 own all H columns)
-      if (s == 0 && (warp & 3) == 0) {
+      if (sl)
+        asm volatile("bar.sync %0, 256;" ::"r"(2 + s) : "memory");
+      else
+        named_sync(1, EPI);
+      // head gradients (warps 0 and 4 of warpgroup 0 own all H columns; with sl each stream's warps
+      // 0 and 4 accumulate its own chunks, combined at the flush)
+      if ((sl || s == 0) && (warp & 3) == 0) {
+        const int q0 = sl ? 4 * s : 0, q1 = sl ? 4 * s + 4 : 8;
 #pragma unroll
         for (int c = 0; c < NCH; ++c) {
           const int col = ch * (H / 2) + c * 32 + lane;
           float a = 0.f;
-#pragma unroll
-          for (int q = 0; q < 8; ++q) a += sU[q] * sHsum[q * (H + 4) + col];
+          for (int q = q0; q < q1; ++q) a += sU[q] * sHsum[q * (H + 4) + col];
           wo_acc[c] += a;
         }
       }
-      if (tid == 0) {
+      if (wt == 0 && (sl || s == 0)) {
+        const int q0 = sl ? 4 * s : 0, q1 = sl ? 4 * s + 4 : 8;
         float a = 0.f;
-        for (int q = 0; q < 8; ++q)
+        for (int q = q0; q < q1; ++q)
           if (gi * 256 + q * 32 < p.nsamp) a += 32.f * sU[q];
         bo_acc += a;
       }
@@ -716,6 +730,17 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
       }
     }
     named_sync(1, EPI);
+    if (sl) {  // stream 1's head partials (its own chunks) onto stream 0's
+      if (s == 1 && (warp & 3) == 0)
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) red[ch * (H / 2) + c * 32 + lane] = wo_acc[c];
+      if (s == 1 && wt == 0) red[H] = bo_acc;
+      named_sync(1, EPI);
+      if (s == 0 && (warp & 3) == 0)
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) wo_acc[c] += red[ch * (H / 2) + c * 32 + lane];
+      if (tid == 0) bo_acc += red[H];
+    }
     if (s == 0 && (warp & 3) == 0) {
 #pragma unroll
       for (int c = 0; c < NCH; ++c) p.head_part[(size_t)blockIdx.x * (H + 1) + ch * (H / 2) + c * 32 + lane] = wo_acc[c];
