@@ -318,18 +318,6 @@ dinr_status launch_rays(dinr_ctx *c, const int64_t *idx, int64_t n, double *rec6
   return DINR_OK;
 }
 
-FieldDev field_dev(const dinr_ctx *c) {
-  FieldDev f;
-  f.C = c->C;
-  f.L = c->L;
-  f.H = c->H;
-  f.mu0 = (float)c->field.mu0;
-  f.B = c->d_B;
-  f.params = c->d_params;
-  f.wpack = c->d_wpack;
-  return f;
-}
-
 template <int H>
 dinr_status launch_tc_mlp(dinr_ctx *c, const Plan &pl, int mode, cudaStream_t st) {
   TcParams p{};

@@ -37,14 +37,6 @@ struct GeomParams {
 // Sample j of the ray sits at a.xyz + (j + u_j) b.xyz: u_j = 1/2 (midpoint rule, R8) or the
 // N3 stratified jitter (philox.cuh).
 
-struct FieldDev {
-  int C, L, H;
-  float mu0;
-  const float *B;        // C x 4
-  const float *params;   // fp32 params (D5)
-  const uint16_t *wpack; // L x (H x H) bf16, SW128 K-major images of W_l ([out][in])
-};
-
 // Launch-bound scratch for the tensor-core backward.
 struct TcScratch {
   uint16_t *hstash;   // L x n_tiles x (H*128) bf16 images of h_l (layer inputs)

@@ -347,7 +347,6 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
     float bo_acc = 0.f, loss_acc = 0.f;
     const int rays_per_group = 256 / p.n_s;
     const int pix_per_group = rays_per_group / p.S;
-    const int chunks_per_ray = p.n_s / 32;
     // every tile holds whole pixels (S N_s <= 128): each stream combines its own pixels, no join.
     // Compiled in for H = 64 only (parallel64: -2.7 %); at H = 128 the extra code cost fan512 +1.9 %
     const bool sl = H == 64 && (128 % (p.S * p.n_s)) == 0;

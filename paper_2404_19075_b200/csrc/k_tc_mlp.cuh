@@ -118,7 +118,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_mlp(TcParams p) {
   const uint32_t a_base = smem_u32(sA), w_base = smem_u32(sW);
   const uint32_t tmem_row = tmem + ((uint32_t)((warp & 3) * 32) << 16);
   const int cg = tid >> 7;                     // column half of this thread
-  const int cb_lo = cg * (H / 64), cb_hi = (cg + 1) * (H / 64);  // its 32-column chunks
+  const int cb_lo = cg * (H / 64);  // first of its H/64 32-column chunks
   float *sMu = reinterpret_cast<float *>(bars + 5);  // [2][128] per-half head partials (forward)
   // the training plan may round the tile count up (paired tiles): padding tiles hold invalid samples
   const int n_tiles = (int)(p.n_tiles > (p.nsamp + 127) / 128 ? p.n_tiles : (p.nsamp + 127) / 128);
