@@ -30,12 +30,15 @@ __device__ __forceinline__ void f2_wait(uint64_t *bar, uint32_t parity) {
   else
     mbar_wait(bar, parity);
 }
+#ifndef DINR_F2_CTL_NS
+#define DINR_F2_CTL_NS 1000
+#endif
 // waits of the MMA-issuer / copy warps: suspended try_wait (DINR_F2_CTL_SPIN: plain spinning)
 __device__ __forceinline__ void f2_ctl_wait(uint64_t *bar, uint32_t parity) {
 #ifdef DINR_F2_CTL_SPIN
   mbar_wait(bar, parity);
 #else
-  mbar_wait_sleep(bar, parity, 1000);
+  mbar_wait_sleep(bar, parity, DINR_F2_CTL_NS);
 #endif
 }
 // operand-tile handoff after the writers' generic-proxy smem writes are fenced:
