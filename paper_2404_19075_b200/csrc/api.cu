@@ -121,16 +121,29 @@ struct Plan {
   float *y_dev, *grad_dev;
 };
 
+constexpr size_t kMaxSmem = 227 * 1024;  // dynamic shared memory per CTA (sm_100)
+
+bool fused2_fits(const dinr_ctx *c) {
+  const size_t smem = c->H == 64 ? Fused2Layout<64>::smem_bytes(c->L) : Fused2Layout<128>::smem_bytes(c->L);
+  return smem <= kMaxSmem;
+}
+
+bool fused1_fits(const dinr_ctx *c) {
+  const size_t smem = c->H == 64 ? FusedLayout<64>::smem_bytes(c->L) : FusedLayout<128>::smem_bytes(c->L);
+  return smem <= kMaxSmem;
+}
+
 bool use_fused(const dinr_ctx *c) {
   static const bool off = std::getenv("DINR_NO_FUSED") != nullptr;
   const int ns = c->geom.samples_per_ray, sn = c->S * ns;
-  return !off && c->field.precision == DINR_BF16 && c->H <= 128 && sn <= 256 && 256 % sn == 0 && (ns & (ns - 1)) == 0;
+  // the fused kernels keep W_1..W_{L-1} resident: deep networks that fit neither take the split path
+  return !off && c->field.precision == DINR_BF16 && c->H <= 128 && sn <= 256 && 256 % sn == 0 && (ns & (ns - 1)) == 0 &&
+         (fused2_fits(c) || fused1_fits(c));
 }
 
 bool use_fused2(const dinr_ctx *c) {
   static const bool off = std::getenv("DINR_FUSED_V1") != nullptr;
-  const size_t smem = c->H == 64 ? Fused2Layout<64>::smem_bytes(c->L) : Fused2Layout<128>::smem_bytes(c->L);
-  return !off && smem <= 227 * 1024;
+  return fused2_fits(c) && !(off && fused1_fits(c));
 }
 
 int loss_blocks_for(int64_t n) { return (int)std::max<int64_t>(1, (n + kLossThreads - 1) / kLossThreads); }

@@ -1,0 +1,76 @@
+"""Randomized gradient/projection parity sweep against the fp64 oracle (test infrastructure; run
+by hand: python tests/_fuzz_parity.py [n_cases] [seed]).  Draws beams, sub-ray layouts, N_s, widths,
+depths, combines and ragged batch sizes, and checks the training step's gradient (1e-2) and the
+projection (2e-3) per case.  Prints one line per case and a summary; exit code 1 on any failure."""
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_2404_19075_b200 import _lib as D  # noqa: E402
+from paper_2404_19075_b200 import synth  # noqa: E402
+from oracle import oracle as O  # noqa: E402
+
+n_cases = int(sys.argv[1]) if len(sys.argv) > 1 else 30
+rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 0)
+dev = torch.device("cuda", 0)
+O.lib()
+
+
+def rel(a, b):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-300))
+
+
+fails = 0
+for k in range(n_cases):
+    name = str(rng.choice(["parallel64", "fan512", "cone512", "cone4d512"]))
+    over = {}
+    if name != "parallel64":
+        over["sub_x"] = int(rng.choice([1, 2, 4]))
+    if name.startswith("cone"):
+        over["sub_z"] = int(rng.choice([1, 2]))
+    over["n_s"] = int(rng.choice([32, 64, 128, 256] if name != "parallel64" else [32, 64, 96]))
+    fover = {"C": int(rng.choice([32, 64, 128])), "L": int(rng.integers(1, 6)),
+             "combine": str(rng.choice(["beer", "linear"]))}
+    n = int(rng.integers(1, 23))
+    g = synth.geometry(name, **over)
+    th, t = synth.views(name, **over)
+    f = synth.field(name, **fover)
+    B = synth.grff_matrix(f["C"], f["sigma_t"], f["sigma_s"], seed=1 + k)
+    prm = synth.init_params(f["C"], f["L"], seed=2 + k)
+    ctx = D.create(0)
+    D.set_geometry(ctx, g, th, t)
+    D.set_field_weights(ctx, f, torch.tensor(B, device=dev), torch.tensor(prm, device=dev))
+    idx = synth.pixel_batch(name, n, seed=100 + k, **over)
+    y, _, _ = O.project_exact(g, th, t, synth.phantom(name), idx, f["combine"])
+    y = y.astype(np.float32)
+    P = synth.param_count(f["C"], f["L"])
+    grad = torch.zeros(P + 1, device=dev)
+    D.project_and_grad(ctx, torch.tensor(idx, device=dev), torch.tensor(y, device=dev), grad)
+    fhat = torch.zeros(n, device=dev)
+    D.project(ctx, torch.tensor(idx, device=dev), fhat)
+    torch.cuda.synchronize()
+    ref, rc = O.project_and_grad(g, th, t, f, B, prm, idx, y)
+    rf, _, _ = O.project(g, th, t, f, B, prm, idx)
+    got = grad.cpu().numpy()
+    H, off, errs = 2 * f["C"], 0, []
+    for _ in range(f["L"]):
+        for m in (H * H, H):
+            errs.append(rel(got[off:off + m], ref[off:off + m]))
+            off += m
+    for m in (H, 1):
+        errs.append(rel(got[off:off + m], ref[off:off + m]))
+        off += m
+    ge, pe = max(errs), rel(fhat.cpu().numpy(), rf)
+    ok = bool(rc == 0 and ge <= 1e-2 and pe <= 2e-3 and abs(got[P] - ref[P]) <= 1e-2 * abs(ref[P]))
+    fails += 0 if ok else 1
+    print(json.dumps({"case": k, "ok": ok, "name": name, "over": over, "field": fover, "n": n,
+                      "path": list(D.train_path(ctx, n)), "grad_err": ge, "proj_err": pe}), flush=True)
+    D.destroy(ctx)
+print(f"{n_cases - fails}/{n_cases} cases within tolerance")
+sys.exit(1 if fails else 0)
