@@ -325,6 +325,25 @@ def test_fused_path_shapes(ctx, dev, O, case):
     assert abs(got[P] - ref[P]) <= 1e-2 * abs(ref[P])
 
 
+@pytest.mark.parametrize("L", [5, 6])
+def test_deep_h128_network_takes_a_path_that_fits(ctx, dev, O, L):
+    """H = 128 with L >= 5: W_1..W_{L-1} no longer fit either fused kernel's shared memory; the
+    step must take the split path (it used to fail in cudaFuncSetAttribute) and stay in tolerance."""
+    g, th, t, f, B, prm = setup_case(ctx, dev, "fan512", {}, dict(L=L), "bf16", "beer")
+    n = 6
+    assert D.train_path(ctx, n)[0] == 0
+    idx = synth.pixel_batch("fan512", n, seed=8)
+    y, _, _ = O.project_exact(g, th, t, synth.phantom("fan512"), idx, "beer")
+    y = y.astype(np.float32)
+    P = synth.param_count(f["C"], f["L"])
+    grad = torch.zeros(P + 1, device=dev)
+    D.project_and_grad(ctx, torch.tensor(idx, device=dev), torch.tensor(y, device=dev), grad)
+    torch.cuda.synchronize()
+    ref, rc = O.project_and_grad(g, th, t, f, B, prm, idx, y)
+    got = grad.cpu().numpy()
+    assert max(tensor_errs(got[:P], ref[:P], f["C"], f["L"])) <= 1e-2
+
+
 @pytest.mark.parametrize("name", ["fan512", "cone512"])
 def test_training_step_is_deterministic(ctx, dev, name):
     """Every reduction has a fixed order (per-CTA partials, fixed-order assembly): the same step
