@@ -352,17 +352,13 @@ dinr_status launch_tc_mlp(dinr_ctx *c, const Plan &pl, int mode, cudaStream_t st
   p.head_part = pl.head_part;
   p.n_tiles = pl.n_tiles;
   p.stash_feat = pl.feat0 ? 0 : 1;
-  // H = 256 training: the forward is k_tc_fwd2 (packed-bf16 convention: W / 2 images, s2 = 2 swish')
-  const bool fwd2 = H == 256 && !std::getenv("DINR_NO_FWD2");
-  p.half_conv = (fwd2 && mode != 0) ? 1 : 0;
-  if (p.half_conv) p.wpack = c->d_wpack_half;
   size_t smem = TcLayout<H>::smem_bytes(c->L, p.resident != 0);
   if (mode == 2) {
     dinr_status s = set_smem(c, k_tc_mlp<H, 2>, smem);
     if (s) return s;
     Launch L_(c, T_BWD, st);
     k_tc_mlp<H, 2><<<pl.grid_tc, kTcThreads, smem, st>>>(p);
-  } else if (mode == 1 && fwd2) {
+  } else if (mode == 1 && H == 256 && !std::getenv("DINR_NO_FWD2")) {
     // two tile streams per CTA, W_l streamed in N-halves (k_tc_fwd2.cuh)
     const size_t sm2 = Fwd2Layout::smem_bytes(c->L);
     dinr_status s = set_smem(c, k_tc_fwd2, sm2);

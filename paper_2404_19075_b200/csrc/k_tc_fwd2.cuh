@@ -7,12 +7,9 @@
 // features [128 h, 128 h + 128)) that both streams consume before the buffer is refilled:
 //   per layer: W_l half 0 -> MMA(s0, h0), MMA(s1, h0); W_l half 1 -> MMA(s0, h1), MMA(s1, h1)
 // so stream 0's epilogue of layer l runs during stream 1's last MMA and the next weight load, and
-// stream 1's during stream 0's next-layer MMAs.  Outputs as k_tc_mlp MODE 1 (ray-chunk sums of M,
-// bulk stores of every layer input h_l to the h stash, 256-bit stores of the backward state), in
-// the fused kernels' packed-bf16 convention: the MMA uses the W_l / 2 image, so the accumulator
-// plus b_l / 2 is y = z / 2 and, per column pair, h = y (1 + tanh y), s2 = 2 swish'(z) =
-// 1 + t + y (1 - t^2) in bf16x2 arithmetic; the state stored is s2 (bf16) for hidden layers and
-// y_{L-1} (fp16) for the top one, and K3 runs its dX chain with W / 2 (TcParams::half_conv).
+// stream 1's during stream 0's next-layer MMAs.  Same math, rounding and outputs as k_tc_mlp
+// MODE 1: ray-chunk sums of M, bulk stores of every layer input h_l (features for l = 0) to the
+// h stash, 256-bit stores of swish'(z_l) (bf16, hidden layers) / z_{L-1} (fp16) to the s2 stash.
 //   warps 0-7: stream 0 epilogue, warps 8-15: stream 1 (thread = sample row x column half)
 //   warp 16 lane 0: weight loads, MMA issue, stash bulk stores
 // TMEM: stream s accumulates in columns [256 s, 256 s + 256).
@@ -67,7 +64,7 @@ __global__ void __launch_bounds__(Fwd2Layout::NT, 1) k_tc_fwd2(TcParams p) {
     fence_mbar_init();
   }
   const int64_t per = (int64_t)H * H + H;
-  for (int i = tid; i < L * H; i += LY::NT) sBias[i] = 0.5f * p.params[(i / H) * per + (int64_t)H * H + (i % H)];  // b / 2
+  for (int i = tid; i < L * H; i += LY::NT) sBias[i] = p.params[(i / H) * per + (int64_t)H * H + (i % H)];
   for (int i = tid; i <= H; i += LY::NT) sWo[i] = p.params[(int64_t)L * per + i];
   for (int i = tid; i < C * 4; i += LY::NT) sB[i] = p.B[i];
   tc_fence_before();
@@ -205,33 +202,36 @@ __global__ void __launch_bounds__(Fwd2Layout::NT, 1) k_tc_fwd2(TcParams p) {
             tmem_ld16(tmem_row + cb * 32 + q16 * 16, v);
             tmem_wait_ld();
             const int col0 = cb * 32 + q16 * 16;
-            uint32_t yb[8], hk[8], s2k[8];
+            float z[16], sg[16];
 #pragma unroll
-            for (int e = 0; e < 8; ++e) {  // y = z / 2 per column pair, packed-bf16 Swish / swish'
-              const float y0 = __uint_as_float(v[2 * e]) + sBias[l * H + col0 + 2 * e];
-              const float y1 = __uint_as_float(v[2 * e + 1]) + sBias[l * H + col0 + 2 * e + 1];
-              if (last) {
-                __half2 hh = __floats2half2_rn(y0, y1);
-                s2k[e] = *reinterpret_cast<uint32_t *>(&hh);  // top layer: y_{L-1} for K3 (fp16)
-              }
-              yb[e] = pack_bf16x2(y0, y1);
-              const uint32_t t = bf2_tanh(yb[e]);
-              hk[e] = bf2_fma(yb[e], t, yb[e]);
-              if (!last) {
-                const uint32_t w = bf2_fma(t, t ^ kBf2Sign, kBf2One);
-                s2k[e] = bf2_fma(yb[e], w, bf2_add(t, kBf2One));
-              }
+            for (int i = 0; i < 16; ++i) {
+              z[i] = __uint_as_float(v[i]) + sBias[l * H + col0 + i];
+              sg[i] = 0.5f + 0.5f * tanh_approx(0.5f * z[i]);
             }
-            // backward state, [16-column chunk][row][32 B] (the layout K3 reads)
-            st_global_v8_hint(p.zstash + ((((size_t)l * p.n_tiles + tile) * (H / 16) + (col0 >> 4)) * 128 + row) * 32, s2k,
-                              pol_z);
+            {  // backward state, [16-column chunk][row][32 B] (the layout K3 reads)
+              uint32_t h8[8];
+#pragma unroll
+              for (int e = 0; e < 8; ++e) {
+                const int i0 = 2 * e;
+                if (last) {
+                  __half2 hh = __floats2half2_rn(z[i0], z[i0 + 1]);
+                  h8[e] = *reinterpret_cast<uint32_t *>(&hh);
+                } else {
+                  h8[e] = pack_bf16x2(sg[i0] * (1.f + z[i0] * (1.f - sg[i0])), sg[i0 + 1] * (1.f + z[i0 + 1] * (1.f - sg[i0 + 1])));
+                }
+              }
+              st_global_v8_hint(p.zstash + ((((size_t)l * p.n_tiles + tile) * (H / 16) + (col0 >> 4)) * 128 + row) * 32, h8,
+                                pol_z);
+            }
             if (!last) {
-              st_shared_v4(a_base + sw128_offset(row, col0, 128), hk[0], hk[1], hk[2], hk[3]);
-              st_shared_v4(a_base + sw128_offset(row, col0 + 8, 128), hk[4], hk[5], hk[6], hk[7]);
+              uint32_t w8[8];
+#pragma unroll
+              for (int e = 0; e < 8; ++e) w8[e] = pack_bf16x2(z[2 * e] * sg[2 * e], z[2 * e + 1] * sg[2 * e + 1]);
+              st_shared_v4(a_base + sw128_offset(row, col0, 128), w8[0], w8[1], w8[2], w8[3]);
+              st_shared_v4(a_base + sw128_offset(row, col0 + 8, 128), w8[4], w8[5], w8[6], w8[7]);
             } else {
 #pragma unroll
-              for (int e = 0; e < 8; ++e)
-                mu_acc += sWo[col0 + 2 * e] * bf16lo(hk[e]) + sWo[col0 + 2 * e + 1] * bf16hi(hk[e]);
+              for (int i = 0; i < 16; ++i) mu_acc += sWo[col0 + i] * (z[i] * sg[i]);
             }
           }
         }

@@ -38,7 +38,6 @@ struct TcParams {
   float *head_part;  // [gridDim.x][H+1]
   int64_t n_tiles;
   int stash_feat;  // MODE 1: store layer 0's input tile (0: the dW GEMM recomputes the features)
-  int half_conv;   // MODE 2 after k_tc_fwd2: the stash holds y_{L-1} = z / 2 and s2 = 2 swish'; wpack = W / 2
   // N4 inference: samples are voxel centres of vg, outputs per voxel to vout (forward only)
   int grid_mode;
   VoxGrid vg;
@@ -360,8 +359,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_mlp(TcParams p) {
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               const float2 zf = __half22float2(*reinterpret_cast<const __half2 *>(&zz[e]));
-              z[8 * q + 2 * e] = p.half_conv ? 2.f * zf.x : zf.x;
-              z[8 * q + 2 * e + 1] = p.half_conv ? 2.f * zf.y : zf.y;
+              z[8 * q + 2 * e] = zf.x;
+              z[8 * q + 2 * e + 1] = zf.y;
             }
           }
           float x[32];
