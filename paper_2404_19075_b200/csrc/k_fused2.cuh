@@ -312,6 +312,7 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
       for (int q = 0; q < 4; ++q) aoff[c][q] = sw128_offset(row, ch * (H / 2) + c * 32 + 8 * q, 128);
     const uint32_t trow = tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(s * H + ch * (H / 2));
     uint32_t accph = 0, sfph = 0;
+    bool acc_pending = false;  // the previous group's last-step commit, consumed lazily
     bool sf_first = true;
 #ifdef DINR_PHASES
     unsigned long long ph_acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0}, ph_t = clock64();
@@ -376,6 +377,12 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
         uint32_t pc[NFC][4], ps[NFC][4];
 #pragma unroll
         for (int fc = 0; fc < NFC; ++fc) grff8(reinterpret_cast<const float4 *>(sB), ch * (C / 2) + 8 * fc, rb, pc[fc], ps[fc]);
+        if (acc_pending) {  // the features above overlapped the previous group's last MMA
+          f2_wait(&acc_full[s], accph);
+          accph ^= 1;
+          tc_fence_after();
+          acc_pending = false;
+        }
         wait_sa();
 #pragma unroll
         for (int fc = 0; fc < NFC; ++fc) {
@@ -687,11 +694,15 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
         }
         PH2(6);
       }
-      // the last step (dW MMA or delta stash store) must retire before A_s is rewritten
+      // the last step (dW MMA or delta stash store) must retire before A_s is rewritten: its commit
+      // is consumed after the next group's features are computed (wait_sa there covers A_s)
+      acc_pending = true;
+      PH2(7);
+    }
+    if (acc_pending) {  // every MMA retired before the TMEM dW accumulators are read out
       f2_wait(&acc_full[s], accph);
       accph ^= 1;
       tc_fence_after();
-      PH2(7);
     }
     // ------------------------------------------------------------ flush per-CTA partials
 #ifdef DINR_PHASES
