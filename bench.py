@@ -201,13 +201,38 @@ def run_reference(args, rank, world):
     return 0
 
 
+# ---------------------------------------------------------------------------- launcher
+def free_port():
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def launch_ranks(args):
+    """`bench.py --gpus N` run without torchrun: re-execute this script under
+    torch.distributed.run, one rank per GPU on this node (the launch the driver uses for N > 1),
+    and return its exit code.  Fails loudly when fewer than N devices are visible."""
+    if not args.launch_dry_run:
+        import torch
+
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            print(f"bench.py --gpus {args.gpus}: only {have} CUDA device(s) visible", file=sys.stderr)
+            return 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 # ---------------------------------------------------------------------------- our arm
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--workload", default="fan512", choices=list(synth.WORKLOADS))
+    ap.add_argument("--workload", default="cone4d2048", choices=list(synth.WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--batch", type=int, default=0, help="pixels per GPU per step (default: workload's)")
     ap.add_argument("--cpu-baseline-seconds", type=float, default=15.0)
@@ -216,12 +241,22 @@ def main():
     ap.add_argument("--combine", default="beer", choices=["beer", "linear"])
     ap.add_argument("--strong", action="store_true",
                     help="strong scaling: the workload's batch is the global batch, split over the ranks")
+    ap.add_argument("--launch-dry-run", action="store_true",
+                    help="spawn the ranks, have each print its rank and world size, and exit (no GPU work)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return launch_ranks(args)
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.launch_dry_run:
+        print(json.dumps({"rank": rank, "world": world, "local_rank": local}), flush=True)
+        return 0
+    if world != args.gpus:
+        print(f"bench.py --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        return 2
     if args.impl == "reference":
         return run_reference(args, rank, world)
 
@@ -261,6 +296,7 @@ def main():
     D.set_field_weights(ctx, f, B, params, stream=stream)
     pdist.init_comm(ctx, rank, world)
     path_kind, path_nf = D.train_path(ctx, n)
+    gemm_layers = D.train_gemm_layers(ctx, n)
 
     # inputs resident in HBM: a pool of distinct per-step batches from this rank's view shard
     pool = 4
@@ -371,15 +407,15 @@ def main():
         fps = flops_per_sample(L, H)
         # per-kernel algorithmic work per launch
         nsamp = n * S * ns
-        fused = path_kind > 0  # k_fused/k_fused2: forward + loss + dX + top-nf dW in one kernel
-        nf = path_nf
-        alg = {
-            "forward": ("tensor", 2.0 * L * H * H * nsamp),
-            "backward": ("tensor", 2.0 * ((L + (L - 1) + nf) if fused else (L - 1)) * H * H * nsamp),
-            "dw": ("tensor", 2.0 * (L - nf) * H * H * nsamp),
+        # algorithmic H x H GEMMs per sample of each kernel class on this path, from the library
+        # (dinr_train_gemm_layers: forward L, dX L - 1, dW L in total; recomputes not counted)
+        gl = gemm_layers
+        assert sum(gl.values()) == 3 * L - 1, gl
+        alg = {k: ("tensor", 2.0 * gl[k] * H * H * nsamp) for k in ("forward", "backward", "dw") if gl[k] > 0}
+        alg.update({
             "rays": ("hbm", n * (8 + S * 36.0)),
             "loss": ("hbm", n * (4 + 4 + S * (4 + 4.0 * (ns // 32)) + S * 4)),
-        }
+        })
         shares = {k: v[0] for k, v in ktimes.items()}
         dom = max((k for k in alg), key=lambda k: shares.get(k, 0.0))
         ms_k, n_k = ktimes[dom]

@@ -268,6 +268,15 @@ int64_t dinr_launch_count(const dinr_ctx *ctx);
  * roofline bookkeeping of bench.py.  DINR_ESTATE before weights are set. */
 dinr_status dinr_train_path(dinr_ctx *ctx, int64_t n, int32_t *fused_kernel, int32_t *fused_dw_layers);
 
+/* Algorithmic work of the training step per kernel class, for the roofline (only
+ * what the method must compute -- L forward, L - 1 dX and L dW H x H GEMMs per sample, i.e.
+ * 2 (3L - 1) H^2 FLOP; recomputed GEMMs and padding are not counted).  gemm_layers[which]
+ * (which = the dinr_read_timing classes 0..7) receives the number of those H x H GEMMs per
+ * sample that the kernels of that class perform for a batch of n pixels on the current path;
+ * the entries sum to 3L - 1.  Host query, no device work.  DINR_ESTATE before weights are set;
+ * DINR_EINVAL for a null array or n < 0. */
+dinr_status dinr_train_gemm_layers(dinr_ctx *ctx, int64_t n, int32_t gemm_layers[8]);
+
 #ifdef __cplusplus
 }
 #endif

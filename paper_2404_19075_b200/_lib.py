@@ -30,6 +30,7 @@ EXPORTS = [
     "dinr_allreduce_grads", "dinr_get_device_status", "dinr_set_timing", "dinr_read_timing",
     "dinr_launch_count", "dinr_adam_step", "dinr_phantom_project", "dinr_set_sampling",
     "dinr_default_grid", "dinr_voxelize", "dinr_voxelize_to_file", "dinr_train_path",
+    "dinr_train_gemm_layers",
 ]
 SAMPLINGS = {"midpoint": 0, "jitter": 1}
 
@@ -105,6 +106,7 @@ def load(path: str = SO_PATH):
         "dinr_set_sampling": (st, [vp, C.c_int, C.c_uint64, C.c_uint32]),
         "dinr_default_grid": (st, [vp, C.POINTER(VoxelGrid)]),
         "dinr_train_path": (st, [vp, i64, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
+        "dinr_train_gemm_layers": (st, [vp, i64, C.POINTER(C.c_int32)]),
         "dinr_voxelize": (st, [vp, C.POINTER(VoxelGrid), C.c_double, i64, i64, vp, vp]),
         "dinr_voxelize_to_file": (st, [vp, C.POINTER(VoxelGrid), i64, i64, C.c_char_p, i64]),
         "dinr_set_field_weights": (st, [vp, C.POINTER(FieldDesc), vp, vp, vp]),
@@ -191,6 +193,13 @@ def train_path(ctx, n: int):
     fk, nf = C.c_int32(), C.c_int32()
     _check(ctx, load().dinr_train_path(ctx, int(n), C.byref(fk), C.byref(nf)))
     return fk.value, nf.value
+
+
+def train_gemm_layers(ctx, n: int) -> dict:
+    """Algorithmic H x H GEMMs per sample done by each timed kernel class (sums to 3L - 1)."""
+    arr = (C.c_int32 * 8)()
+    _check(ctx, load().dinr_train_gemm_layers(ctx, int(n), arr))
+    return {k: arr[v] for k, v in TIMERS.items()}
 
 
 def default_grid(ctx) -> dict:

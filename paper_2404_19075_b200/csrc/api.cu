@@ -932,10 +932,12 @@ dinr_status dinr_adam_step(dinr_ctx *c, float *params, const float *grad, float 
   CUDA_TRY(c, cudaSetDevice(c->device));
   cudaStream_t st = (cudaStream_t)stream;
   const float c1 = (float)(1.0 - std::pow(b1, (double)step)), c2 = (float)(1.0 - std::pow(b2, (double)step));
+  const bool bf16 = c->field.precision == DINR_BF16;  // FP32_VERIFY widths need not be multiples of 64
   Launch L_(c, T_PACK, st);
   k_adam_pack<<<(unsigned)((c->P + 255) / 256), 256, 0, st>>>(params, grad, m, v, c->P, c->H, c->L, (float)lr,
                                                               (float)b1, (float)b2, (float)eps, c1, c2, c->d_params,
-                                                              c->d_wpack, c->d_wpack_half);
+                                                              bf16 ? c->d_wpack : nullptr,
+                                                              bf16 ? c->d_wpack_half : nullptr);
   CUDA_TRY(c, cudaGetLastError());
   return DINR_OK;
 }
@@ -1126,6 +1128,31 @@ dinr_status dinr_train_path(dinr_ctx *c, int64_t n, int32_t *fused_kernel, int32
   plan_layout(c, std::max<int64_t>(n, 1), true, false, pl, nullptr);
   *fused_kernel = pl.fused ? (pl.fused2 ? 2 : 1) : 0;
   *fused_dw_layers = pl.fused ? pl.nf : 0;
+  return DINR_OK;
+}
+
+dinr_status dinr_train_gemm_layers(dinr_ctx *c, int64_t n, int32_t *gl) {
+  if (!c || !gl || n < 0) return c ? fail(c, DINR_EINVAL, "null array or n < 0") : DINR_EINVAL;
+  if (!c->have_geom || !c->have_field) return fail(c, DINR_ESTATE, "geometry and field weights must be set first");
+  Plan pl;
+  plan_layout(c, std::max<int64_t>(n, 1), true, false, pl, nullptr);
+  const int L = c->L;
+  for (int k = 0; k < T_N; ++k) gl[k] = 0;
+  if (c->field.precision == DINR_FP32_VERIFY) {  // SIMT verify path: forward, backward (dX + dW)
+    gl[T_FWD] = L;
+    gl[T_BWD] = (L - 1) + L;
+  } else if (pl.fused) {
+    // one fused kernel: forward, the dX chain down to layer lmin + 1, the TMEM-fused dW of the top
+    // nf layers; k_dw01 (dw01): dW of layers 0 and 1 plus layer 1's dX (its layer-0 forward is a
+    // recompute); otherwise K5: dW of the nu lower layers
+    const int lmin = pl.dw01 ? 1 : 0;
+    gl[T_BWD] = L + (L - 1 - lmin) + pl.nf;
+    gl[T_DW] = pl.nu + lmin;
+  } else {  // split path: K2 forward, K3 dX chain, K5 dW
+    gl[T_FWD] = L;
+    gl[T_BWD] = L - 1;
+    gl[T_DW] = L;
+  }
   return DINR_OK;
 }
 

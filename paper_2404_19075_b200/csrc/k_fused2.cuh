@@ -354,6 +354,12 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
     // every tile holds whole pixels (S N_s <= 128): each stream combines its own pixels, no join.
     // Compiled in for H = 64 only (parallel64: -2.7 %); at H = 128 the extra code cost fan512 +1.9 %
     const bool sl = H == 64 && (128 % (p.S * p.n_s)) == 0;
+    // loss operands: with sl each stream loads and stores its own tile's rays and pixels, so the
+    // per-stream barrier orders them (stream 0 may start group gi+1 while stream 1 still forms the
+    // loss of group gi when nothing else holds it back, e.g. L = 1); otherwise threads of stream 0
+    // cover the group and the join barrier orders them
+    const int pre_r = sl ? rays_per_group >> 1 : rays_per_group, pre_p = sl ? pix_per_group >> 1 : pix_per_group;
+    const int pre_t = sl ? wt : tid, pre_ro = sl ? s * pre_r : 0, pre_po = sl ? s * pre_p : 0;
 
     for (int64_t gi = blockIdx.x; gi < n_groups; gi += gridDim.x) {
       const int64_t tile = 2 * gi + s;
@@ -362,12 +368,12 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
       // loss operands of the group's pixels (quadrature weights, measured data), fetched now so
       // that the loss phase -- where both streams wait -- has no global-memory latency
       float wq_pre = 0.f, y_pre = 0.f;  // loads in flight during the feature computation
-      if (tid < pix_per_group * p.S) {
-        const int64_t ray = gi * pix_per_group * p.S + tid;
+      if (pre_t < pre_r) {
+        const int64_t ray = gi * rays_per_group + pre_ro + pre_t;
         if (ray < p.n_pix * p.S) wq_pre = p.rec32[2 * ray + 1].w;
       }
-      if (tid < pix_per_group) {
-        const int64_t pix = gi * pix_per_group + tid;
+      if (pre_t < pre_p) {
+        const int64_t pix = gi * pix_per_group + pre_po + pre_t;
         if (pix < p.n_pix) y_pre = p.y[pix];
       }
       // ------------------------------------------------------------ a5/a6 features
@@ -392,8 +398,8 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
         }
       }
       fence_proxy_async_smem();
-      if (tid < pix_per_group * p.S) sWq[tid] = wq_pre;
-      if (tid < pix_per_group) sY[tid] = y_pre;
+      if (pre_t < pre_r) sWq[pre_ro + pre_t] = wq_pre;
+      if (pre_t < pre_p) sY[pre_po + pre_t] = y_pre;
       PH2(0);
       f2_arrive_tile(&a_full[s], s);
       // ------------------------------------------------------------ a7/a8 forward layers

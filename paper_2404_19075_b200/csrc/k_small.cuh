@@ -150,7 +150,8 @@ __global__ void k_adam_pack(float *__restrict__ params, const float *__restrict_
   params[q] = w;
   ctx_params[q] = w;
   const int64_t per = (int64_t)H * H + H;
-  if (q < (int64_t)L * per) {
+  // the bf16 SW128 images exist only for the BF16 path (H in {64,128,256}); FP32_VERIFY passes null
+  if (wpack && q < (int64_t)L * per) {
     const int l = (int)(q / per);
     const int64_t e = q - (int64_t)l * per;
     if (e < (int64_t)H * H) {

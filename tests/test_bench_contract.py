@@ -50,7 +50,7 @@ def test_our_arm_line():
         pytest.skip("no CUDA device")
     d = run_bench("--steps", "3", "--warmup", "3", "--cpu-baseline-seconds", "1")
     common_keys(d)
-    assert d["config"]["workload"] == "fan512" and d["n_gpus"] == 1 and d["scaling"] == "weak"
+    assert d["config"]["workload"] == "cone4d2048" and d["n_gpus"] == 1 and d["scaling"] == "weak"
     assert d["dtype"] == "bf16" and d["data"] == "synthetic" and "l2" in d["config"]
     r = d["roofline"]
     for k in ("bound", "achieved", "peak", "unit", "frac", "traffic"):
@@ -65,3 +65,21 @@ def test_our_arm_line():
     for k in ("sm_mhz", "sm_max_mhz", "reasons"):
         assert k in d["clocks"], k
     assert d["replicas_equal"] is True
+
+
+def test_launcher_spawns_one_rank_per_gpu():
+    """`bench.py --gpus 2` without torchrun re-executes itself under torch.distributed.run with
+    two ranks (dry run: each rank reports its RANK / WORLD_SIZE and exits, no GPU needed)."""
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--launch-dry-run"],
+                         capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    ranks = [json.loads(ln) for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert sorted(r["rank"] for r in ranks) == [0, 1]
+    assert all(r["world"] == 2 for r in ranks)
+
+
+def test_world_mismatch_fails_loudly():
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2"], capture_output=True,
+                         text=True, timeout=300, cwd=ROOT, env=env)
+    assert out.returncode != 0 and "WORLD_SIZE" in out.stderr

@@ -1,6 +1,6 @@
 """Multi-process (world_size 2, gloo, CPU) tests of the data-parallel host logic:
 view-sharded batches are disjoint and cover only the rank's views, the NCCL unique id is
-broadcast identically, and averaging per-rank oracle gradients equals the gradient of the
+broadcast identically (the id comes from the library's dinr_nccl_unique_id), and averaging per-rank oracle gradients equals the gradient of the
 union batch (K-invariance, R16)."""
 import os
 import socket
@@ -33,9 +33,11 @@ def _worker(rank, world, port, out_q):
         from paper_2404_19075_b200 import dist as pd
         from paper_2404_19075_b200 import synth
 
-        # 1) unique-id broadcast
-        uid = pd.broadcast_unique_id(lambda: bytes(np.random.default_rng(7).integers(0, 256, 128, dtype=np.uint8)),
-                                     rank, world)
+        # 1) unique-id broadcast of the library's own NCCL id (dinr_nccl_unique_id: ncclGetUniqueId
+        #    needs no GPU), exactly as dist.init_comm does before dinr_comm_init
+        from paper_2404_19075_b200 import _lib as D
+
+        uid = pd.broadcast_unique_id(D.nccl_unique_id, rank, world)
         ids = [None] * world
         dist.all_gather_object(ids, uid)
         # 2) shards
@@ -76,8 +78,9 @@ def test_two_rank_gloo(O):
         p.join(timeout=60)
         assert p.exitcode == 0
     res.sort(key=lambda r: r[0])
-    # identical ids everywhere
+    # identical ids everywhere (128 bytes from rank 0's ncclGetUniqueId, not all zero)
     assert res[0][1][0] == res[0][1][1] == res[1][1][0]
+    assert len(res[0][1][0]) == 128 and any(res[0][1][0])
     # each rank drew only from its own views, and the shards are disjoint
     for r in range(world):
         assert res[r][2] == {r}
