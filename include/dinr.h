@@ -211,6 +211,58 @@ dinr_status dinr_adam_step(dinr_ctx *ctx, float *params_dev, const float *grad_d
                            int64_t count, double lr, double beta1, double beta2, double eps, int64_t step,
                            void *stream);
 
+/* ---- N1 epoch loop (lr schedule P:540-542; reading R27 in DESIGN.md) ----------
+ * Each process k draws |Omega_k| = batch pixels per iteration (eq:localoptfunc, eq:totbatch:
+ * Omega* = world * batch), without replacement through a per-epoch pseudo-random permutation
+ * (SPEC S:389), computes the local mean loss and gradient, the gradients are averaged
+ * over the processes (dinr_allreduce_grads), and every process applies the same Adam step with
+ * lr = lr0 * lr_decay^epoch.  One epoch = ceil(M N / Omega*) iterations; the last
+ * iteration of an epoch wraps to the start of the same permutation so that every process always
+ * takes exactly `batch` pixels (equal |Omega_k|).
+ * sharding DINR_SHARD_VIEWS: process `rank` owns views rank, rank + world, ... and
+ *   permutes the nv N positions of its shard (nv = ceil((M - rank) / world)); its y source is that
+ *   shard, nv N floats stored view by view.
+ * sharding DINR_SHARD_GLOBAL: one permutation of all M N pixels, each iteration's Omega* positions
+ *   split contiguously over the processes; the y source is all M N floats.
+ * The permutation: an 8-round Feistel network over Philox4x32-10 with cycle walking (k_sampler.cuh;
+ * the oracle implements the same generator independently). */
+typedef enum { DINR_SHARD_VIEWS = 0, DINR_SHARD_GLOBAL = 1 } dinr_sharding;
+
+typedef struct {
+  uint64_t seed;    /* permutation key */
+  int32_t rank;     /* this process (0 <= rank < world) */
+  int32_t world;    /* number of processes K; > 1 requires dinr_comm_init with the same world */
+  int32_t sharding; /* dinr_sharding */
+  int32_t reserved; /* 0 */
+  int64_t batch;    /* |Omega_k| >= 1 */
+  double lr0;       /* initial learning rate (paper: 0.001) */
+  double lr_decay;  /* per-epoch factor (paper: 0.95) */
+  double beta1, beta2, eps; /* Adam (0.9, 0.999, 1e-8) */
+} dinr_train_desc;
+
+/* ceil(M N / (world * batch)).  DINR_ESTATE before dinr_set_geometry; DINR_EINVAL for a bad desc. */
+dinr_status dinr_iterations_per_epoch(dinr_ctx *ctx, const dinr_train_desc *desc, int64_t *out);
+
+/* The batch of iteration `iteration` of epoch `epoch` for desc->rank: idx_dev[batch] pixel
+ * indices and, when y_src_dev is not null, y_dev[batch] = the measured values gathered from the
+ * y source described above.  Stream-ordered, one kernel.  DINR_EINVAL for negative epoch /
+ * iteration, a bad desc or null outputs. */
+dinr_status dinr_sample_batch(dinr_ctx *ctx, const dinr_train_desc *desc, int64_t epoch, int64_t iteration,
+                              const float *y_src_dev, int64_t *idx_dev, float *y_dev, void *stream);
+
+/* Runs global iterations first .. first + count - 1 (iteration g is iteration g mod I of epoch
+ * g / I, I = dinr_iterations_per_epoch; Adam step g + 1): sample, dinr_project_and_grad,
+ * dinr_allreduce_grads when world > 1, dinr_adam_step with the epoch's lr.  params_dev, m_dev,
+ * v_dev: P fp32 (caller-owned, updated in place; the context's weight images follow them);
+ * grad_dev: P + 1 fp32 scratch (holds the last averaged gradient and loss on return);
+ * loss_dev: count fp32, the global mean loss of each iteration (eq:localoptfunc averaged over
+ * the processes).  All stream-ordered on `stream`, no host synchronization.  Requires
+ * dinr_set_field_weights (DINR_ESTATE), and dinr_comm_init with desc->world processes when
+ * world > 1 (DINR_ESTATE). */
+dinr_status dinr_train_iterations(dinr_ctx *ctx, const dinr_train_desc *desc, int64_t first, int64_t count,
+                                  const float *y_src_dev, float *params_dev, float *m_dev, float *v_dev,
+                                  float *grad_dev, float *loss_dev, void *stream);
+
 /* Analytic phantom primitive (NEXT row N2): kind 0 = indicator ellipsoid (value mu), 1 = smooth
  * ellipsoid mu_c (1 - rho^2)^2, 2 = Gaussian A exp(-rho^2/2) with sigmas = axes.  Axis-aligned in
  * the object frame, centre(t) = center + velocity t, axes(t) = axes + axes_rate t. */

@@ -723,3 +723,56 @@ void or_adam_step(double *param, const double *grad, double *m, double *v, int64
     param[q] -= lr * mh / (sqrt(vh) + eps);
   }
 }
+
+/* ---------------------------------------------------------------- N1 sampler (R27) */
+int64_t or_perm(int64_t D, uint64_t seed, int64_t epoch, int64_t q) {
+  int h = 1;
+  while (((uint64_t)1 << (2 * h)) < (uint64_t)D) ++h;
+  const uint64_t mask = ((uint64_t)1 << h) - 1;
+  const uint32_t key[2] = {(uint32_t)(seed & 0xFFFFFFFFu), (uint32_t)(seed >> 32) ^ 0x9E3779B9u};
+  uint64_t x = (uint64_t)q;
+  do {
+    uint64_t lh = x >> h, rh = x & mask;
+    for (uint32_t r = 0; r < 8; ++r) {
+      uint32_t ctr[4] = {(uint32_t)rh, r, (uint32_t)((uint64_t)epoch & 0xFFFFFFFFu), (uint32_t)((uint64_t)epoch >> 32)};
+      uint32_t out[4];
+      or_philox4x32(ctr, key, out);
+      uint64_t nl = rh, nr = lh ^ ((uint64_t)out[0] & mask);
+      lh = nl;
+      rh = nr;
+    }
+    x = (lh << h) | rh;
+  } while (x >= (uint64_t)D);
+  return (int64_t)x;
+}
+
+int64_t or_iterations_per_epoch(int64_t M, int64_t N, int world, int64_t n) {
+  const int64_t per = (int64_t)world * n;
+  return (M * N + per - 1) / per;
+}
+
+int or_sample_batch(int64_t M, int64_t N, uint64_t seed, int64_t epoch, int64_t it, int rank, int world, int mode,
+                    int64_t n, int64_t *idx, int64_t *src) {
+  if (M < 1 || N < 1 || world < 1 || rank < 0 || rank >= world || n < 0 || epoch < 0 || it < 0) return -1;
+  if (mode == 0) {
+    const int64_t nv = (M - rank + world - 1) / world;
+    if (nv < 1) return -1;
+    const int64_t D = nv * N;
+    for (int64_t j = 0; j < n; ++j) {
+      const int64_t p = (it * n + j) % D;
+      const int64_t q = or_perm(D, seed, epoch, p);
+      const int64_t view = rank + (int64_t)world * (q / N);
+      idx[j] = view * N + q % N;
+      src[j] = q;
+    }
+  } else if (mode == 1) {
+    const int64_t D = M * N;
+    for (int64_t j = 0; j < n; ++j) {
+      const int64_t p = (it * world * n + (int64_t)rank * n + j) % D;
+      idx[j] = src[j] = or_perm(D, seed, epoch, p);
+    }
+  } else {
+    return -1;
+  }
+  return 0;
+}

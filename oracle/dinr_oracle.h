@@ -148,6 +148,26 @@ int or_project_exact(const or_geom *g, const double *theta, const double *t, int
 void or_adam_step(double *param, const double *grad, double *m, double *v, int64_t n, double lr, double b1,
                   double b2, double eps, int64_t step);
 
+/* N1 sampler ("we randomly choose a subset Omega_k"; epochs P:3333-3336; without
+ * replacement via a per-epoch permutation; reading R27 in DESIGN.md).
+ * or_perm: the bijection perm_e of [0, D) for epoch e -- an 8-round balanced Feistel network on 2h
+ * bits (h >= 1 smallest with 4^h >= D), x = (Lh << h) | Rh, round r: (Lh, Rh) <- (Rh, Lh ^ (F_r(Rh)
+ * & (2^h - 1))), F_r(R) = Philox4x32-10(ctr = (R, r, e lo, e hi), key = (seed lo, seed hi ^
+ * 0x9E3779B9)) word 0; applied again while the value is >= D (cycle walking). */
+int64_t or_perm(int64_t D, uint64_t seed, int64_t epoch, int64_t q);
+/* Iteration `it` of epoch `epoch` on process `rank` of `world`, n pixels each (eq:totbatch).
+ * mode 0 (view shards): the shard holds views rank, rank + world, ... (nv = ceil((M -
+ * rank) / world)), D = nv N; p_j = (it n + j) mod D, q = perm_e(p_j), idx = (rank + world (q / N)) N +
+ * q mod N, src = q (the pixel's position in the rank's y shard, stored view by view).
+ * mode 1 (one global permutation split contiguously over the processes): D = M N;
+ * p_j = (it world n + rank n + j) mod D, idx = src = perm_e(p_j).
+ * The last iteration of an epoch wraps to the start of the same permutation, so every process
+ * always takes exactly n pixels (R27).  Returns 0, or -1 for bad arguments. */
+int or_sample_batch(int64_t M, int64_t N, uint64_t seed, int64_t epoch, int64_t it, int rank, int world, int mode,
+                    int64_t n, int64_t *idx, int64_t *src);
+/* Iterations per epoch: ceil(M N / (world n)). */
+int64_t or_iterations_per_epoch(int64_t M, int64_t N, int world, int64_t n);
+
 #ifdef __cplusplus
 }
 #endif

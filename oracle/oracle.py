@@ -88,6 +88,11 @@ def lib():
         _lib.or_default_grid.argtypes = [C.POINTER(OrGeom), C.POINTER(OrGrid)]
         _lib.or_voxelize.argtypes = [C.POINTER(OrGeom), C.POINTER(OrField), d, d, C.POINTER(OrGrid), C.c_double, i64, i64,
                                      d]
+        _lib.or_perm.restype = C.c_int64
+        _lib.or_perm.argtypes = [i64, C.c_uint64, i64, i64]
+        _lib.or_sample_batch.argtypes = [i64, i64, C.c_uint64, i64, i64, C.c_int, C.c_int, C.c_int, i64, pi64, pi64]
+        _lib.or_iterations_per_epoch.restype = C.c_int64
+        _lib.or_iterations_per_epoch.argtypes = [i64, i64, C.c_int, i64]
         _lib.or_line_integral_exact.restype = C.c_double
         _lib.or_line_integral_exact.argtypes = [C.POINTER(OrPrim), i32, d, d, C.c_double, C.c_double, C.c_double]
     return _lib
@@ -291,3 +296,59 @@ def adam_step(param, grad, m, v, lr, b1=0.9, b2=0.999, eps=1e-8, step=1):
     gg = _f64(grad)
     lib().or_adam_step(_dp(pr), _dp(gg), _dp(mm), _dp(vv), len(pr), lr, b1, b2, eps, step)
     return pr, mm, vv
+
+
+# ---------------------------------------------------------------- N1: sampler + epoch loop
+SHARDINGS = {"views": 0, "global": 1}
+
+
+def perm(D, seed, epoch, q):
+    """perm_e(q): the epoch's bijection of [0, D) (Feistel + cycle walking, R27)."""
+    return int(lib().or_perm(int(D), int(seed), int(epoch), int(q)))
+
+
+def iterations_per_epoch(M, N, world, n):
+    """ceil(M N / (world n))."""
+    return int(lib().or_iterations_per_epoch(int(M), int(N), int(world), int(n)))
+
+
+def sample_batch(M, N, seed, epoch, it, rank, world, n, sharding="views"):
+    """(pixel indices, positions in the y source) of iteration `it` of epoch `epoch` on `rank`."""
+    idx = np.zeros(n, dtype=np.int64)
+    src = np.zeros(n, dtype=np.int64)
+    p64 = C.POINTER(C.c_int64)
+    rc = lib().or_sample_batch(int(M), int(N), int(seed), int(epoch), int(it), int(rank), int(world),
+                               SHARDINGS[sharding], int(n), idx.ctypes.data_as(p64), src.ctypes.data_as(p64))
+    if rc != 0:
+        raise ValueError("or_sample_batch: bad arguments")
+    return idx, src
+
+
+def train(g, theta, t, f, B, params, y_src, seed, n, world, iterations, sharding="views", lr0=1e-3, decay=0.95,
+          b1=0.9, b2=0.999, eps=1e-8, first=0):
+    """The paper's distributed stochastic optimization, all K = world processes
+    emulated in turn: per iteration every process samples its n pixels, computes its local mean
+    loss and gradient (eq:localoptfunc), the gradients and losses are averaged in rank order (O13),
+    and one replicated Adam step is taken with lr = lr0 decay^epoch.  y_src[r] is rank
+    r's y source (its view shard for sharding="views", the full M N array for "global").  Returns
+    (params, per-iteration mean losses) in fp64."""
+    M, N = len(theta), g["n_rows"] * g["n_cols"]
+    ipe = iterations_per_epoch(M, N, world, n)
+    P = len(params)
+    prm = _f64(params).copy()
+    m, v = np.zeros(P), np.zeros(P)
+    losses = []
+    for gi in range(first, first + iterations):
+        epoch, it = divmod(gi, ipe)
+        grads = []
+        for r in range(world):
+            idx, src = sample_batch(M, N, seed, epoch, it, r, world, n, sharding)
+            y = np.asarray(y_src[r])[src]
+            gr, rc = project_and_grad(g, theta, t, f, B, prm, idx, y)
+            if rc != 0:
+                raise RuntimeError("oracle project_and_grad failed")
+            grads.append(gr)
+        avg = allreduce_mean(grads)
+        losses.append(float(avg[P]))
+        prm, m, v = adam_step(prm, avg[:P], m, v, lr0 * decay ** epoch, b1, b2, eps, gi + 1)
+    return prm, np.array(losses)

@@ -30,8 +30,9 @@ EXPORTS = [
     "dinr_allreduce_grads", "dinr_get_device_status", "dinr_set_timing", "dinr_read_timing",
     "dinr_launch_count", "dinr_adam_step", "dinr_phantom_project", "dinr_set_sampling",
     "dinr_default_grid", "dinr_voxelize", "dinr_voxelize_to_file", "dinr_train_path",
-    "dinr_train_gemm_layers",
+    "dinr_train_gemm_layers", "dinr_iterations_per_epoch", "dinr_sample_batch", "dinr_train_iterations",
 ]
+SHARDINGS = {"views": 0, "global": 1}
 SAMPLINGS = {"midpoint": 0, "jitter": 1}
 
 
@@ -73,6 +74,18 @@ class FieldDesc(C.Structure):
                 ("precision", C.c_int32), ("reserved", C.c_int32), ("mu0", C.c_double)]
 
 
+class TrainDesc(C.Structure):
+    _fields_ = [("seed", C.c_uint64), ("rank", C.c_int32), ("world", C.c_int32), ("sharding", C.c_int32),
+                ("reserved", C.c_int32), ("batch", C.c_int64), ("lr0", C.c_double), ("lr_decay", C.c_double),
+                ("beta1", C.c_double), ("beta2", C.c_double), ("eps", C.c_double)]
+
+
+def train_desc(seed, batch, rank=0, world=1, sharding="views", lr0=1e-3, lr_decay=0.95, beta1=0.9, beta2=0.999,
+               eps=1e-8) -> TrainDesc:
+    return TrainDesc(int(seed), int(rank), int(world), SHARDINGS[sharding], 0, int(batch), float(lr0),
+                     float(lr_decay), float(beta1), float(beta2), float(eps))
+
+
 _lib = None
 
 
@@ -107,6 +120,9 @@ def load(path: str = SO_PATH):
         "dinr_default_grid": (st, [vp, C.POINTER(VoxelGrid)]),
         "dinr_train_path": (st, [vp, i64, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
         "dinr_train_gemm_layers": (st, [vp, i64, C.POINTER(C.c_int32)]),
+        "dinr_iterations_per_epoch": (st, [vp, C.POINTER(TrainDesc), C.POINTER(C.c_int64)]),
+        "dinr_sample_batch": (st, [vp, C.POINTER(TrainDesc), i64, i64, vp, vp, vp, vp]),
+        "dinr_train_iterations": (st, [vp, C.POINTER(TrainDesc), i64, i64, vp, vp, vp, vp, vp, vp, vp]),
         "dinr_voxelize": (st, [vp, C.POINTER(VoxelGrid), C.c_double, i64, i64, vp, vp]),
         "dinr_voxelize_to_file": (st, [vp, C.POINTER(VoxelGrid), i64, i64, C.c_char_p, i64]),
         "dinr_set_field_weights": (st, [vp, C.POINTER(FieldDesc), vp, vp, vp]),
@@ -200,6 +216,28 @@ def train_gemm_layers(ctx, n: int) -> dict:
     arr = (C.c_int32 * 8)()
     _check(ctx, load().dinr_train_gemm_layers(ctx, int(n), arr))
     return {k: arr[v] for k, v in TIMERS.items()}
+
+
+def iterations_per_epoch(ctx, desc: TrainDesc) -> int:
+    """N1: ceil(M N / (world * batch))."""
+    out = C.c_int64()
+    _check(ctx, load().dinr_iterations_per_epoch(ctx, C.byref(desc), C.byref(out)))
+    return out.value
+
+
+def sample_batch(ctx, desc: TrainDesc, epoch: int, iteration: int, idx, y_src=None, y=None, stream=None):
+    """N1: the batch of (epoch, iteration) for desc.rank into idx (int64[batch]) and, with a y
+    source, the gathered measurements into y (float32[batch])."""
+    _check(ctx, load().dinr_sample_batch(ctx, C.byref(desc), int(epoch), int(iteration),
+                                         _ptr(y_src) if y_src is not None else None, _ptr(idx),
+                                         _ptr(y) if y is not None else None, _stream(stream, idx)))
+
+
+def train_iterations(ctx, desc: TrainDesc, first: int, count: int, y_src, params, m, v, grad, loss, stream=None):
+    """N1: global iterations first .. first + count - 1 of the epoch loop (sample, local loss and
+    gradient, all-reduce, Adam at lr0 decay^epoch); loss[count] receives each iteration's mean loss."""
+    _check(ctx, load().dinr_train_iterations(ctx, C.byref(desc), int(first), int(count), _ptr(y_src), _ptr(params),
+                                             _ptr(m), _ptr(v), _ptr(grad), _ptr(loss), _stream(stream, params)))
 
 
 def default_grid(ctx) -> dict:

@@ -26,6 +26,7 @@
 #include "k_tc_fwd2.cuh"
 #include "k_infer.cuh"
 #include "k_phantom.cuh"
+#include "k_sampler.cuh"
 #include "nccl_dl.cuh"
 
 using namespace dinr;
@@ -939,6 +940,120 @@ dinr_status dinr_adam_step(dinr_ctx *c, float *params, const float *grad, float 
                                                               bf16 ? c->d_wpack : nullptr,
                                                               bf16 ? c->d_wpack_half : nullptr);
   CUDA_TRY(c, cudaGetLastError());
+  return DINR_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+// N1: the validated shape of a dinr_train_desc for this context (see include/dinr.h)
+dinr_status train_desc_check(dinr_ctx *c, const dinr_train_desc *d, int64_t *D, int64_t *ipe) {
+  if (!d) return fail(c, DINR_EINVAL, "null train desc");
+  if (!c->have_geom) return fail(c, DINR_ESTATE, "dinr_set_geometry must be called first");
+  if (d->world < 1 || d->rank < 0 || d->rank >= d->world || d->batch < 1 ||
+      (d->sharding != DINR_SHARD_VIEWS && d->sharding != DINR_SHARD_GLOBAL) || !(d->lr0 >= 0) ||
+      !(d->lr_decay > 0) || !(d->beta1 >= 0 && d->beta1 < 1) || !(d->beta2 >= 0 && d->beta2 < 1) || !(d->eps > 0))
+    return fail(c, DINR_EINVAL, "bad train desc (0 <= rank < world, batch >= 1, sharding, lr0 >= 0, lr_decay > 0, "
+                                "0 <= beta < 1, eps > 0)");
+  const int64_t N = (int64_t)c->geom.n_rows * c->geom.n_cols;
+  if (d->sharding == DINR_SHARD_VIEWS) {
+    const int64_t nv = (c->M - d->rank + d->world - 1) / d->world;
+    if (nv < 1) return fail(c, DINR_EINVAL, "view sharding: more processes than views");
+    *D = nv * N;
+  } else {
+    *D = c->M * N;
+  }
+  const int64_t per = (int64_t)d->world * d->batch;
+  *ipe = (c->M * N + per - 1) / per;
+  return DINR_OK;
+}
+
+dinr_status launch_sample(dinr_ctx *c, const dinr_train_desc *d, int64_t D, int64_t epoch, int64_t it,
+                          const float *y_src, int64_t *idx, float *y, cudaStream_t st) {
+  SampleArgs a;
+  a.N = (int64_t)c->geom.n_rows * c->geom.n_cols;
+  a.D = D;
+  a.n = d->batch;
+  // it * world * batch <= M N + world * batch for any iteration of an epoch; the caller's
+  // iteration index is reduced mod the shard first, so the sum cannot overflow
+  const int64_t per = d->sharding == DINR_SHARD_VIEWS ? d->batch : (int64_t)d->world * d->batch;
+  const int64_t off = d->sharding == DINR_SHARD_VIEWS ? 0 : (int64_t)d->rank * d->batch;
+  a.base = (int64_t)(((unsigned __int128)(uint64_t)it * (uint64_t)per + (uint64_t)off) % (uint64_t)D);
+  int h = 1;
+  while ((1ull << (2 * h)) < (uint64_t)D) ++h;
+  a.h = h;
+  a.mode = d->sharding;
+  a.rank = d->rank;
+  a.world = d->world;
+  a.key = make_uint2((uint32_t)d->seed, (uint32_t)(d->seed >> 32) ^ 0x9E3779B9u);
+  a.e_lo = (uint32_t)epoch;
+  a.e_hi = (uint32_t)((uint64_t)epoch >> 32);
+  a.y_src = y_src;
+  a.idx = idx;
+  a.y = y;
+  Launch L_(c, T_RAYS, st);
+  k_sample_batch<<<(unsigned)((d->batch + 255) / 256), 256, 0, st>>>(a);
+  CUDA_TRY(c, cudaGetLastError());
+  return DINR_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+dinr_status dinr_iterations_per_epoch(dinr_ctx *c, const dinr_train_desc *d, int64_t *out) {
+  if (!c || !out) return c ? fail(c, DINR_EINVAL, "null argument") : DINR_EINVAL;
+  int64_t D, ipe;
+  dinr_status s = train_desc_check(c, d, &D, &ipe);
+  if (s) return s;
+  *out = ipe;
+  return DINR_OK;
+}
+
+dinr_status dinr_sample_batch(dinr_ctx *c, const dinr_train_desc *d, int64_t epoch, int64_t it, const float *y_src,
+                              int64_t *idx, float *y, void *stream) {
+  if (!c) return DINR_EINVAL;
+  if (!idx || (y_src && !y) || epoch < 0 || it < 0) return fail(c, DINR_EINVAL, "bad arguments");
+  int64_t D, ipe;
+  dinr_status s = train_desc_check(c, d, &D, &ipe);
+  if (s) return s;
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  return launch_sample(c, d, D, epoch, it, y_src, idx, y, (cudaStream_t)stream);
+}
+
+dinr_status dinr_train_iterations(dinr_ctx *c, const dinr_train_desc *d, int64_t first, int64_t count,
+                                  const float *y_src, float *params, float *m, float *v, float *grad, float *loss,
+                                  void *stream) {
+  if (!c) return DINR_EINVAL;
+  if (!c->have_field) return fail(c, DINR_ESTATE, "dinr_set_field_weights must be called first");
+  if (first < 0 || count < 0 || !y_src || !params || !m || !v || !grad || (count > 0 && !loss))
+    return fail(c, DINR_EINVAL, "bad arguments");
+  int64_t D, ipe;
+  dinr_status s = train_desc_check(c, d, &D, &ipe);
+  if (s) return s;
+  if (d->world > 1 && (!c->comm || c->world != d->world || c->rank != d->rank))
+    return fail(c, DINR_ESTATE, "world > 1 needs dinr_comm_init with the same rank and world");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  for (int64_t g = first; g < first + count; ++g) {
+    const int64_t epoch = g / ipe, it = g % ipe;
+    Plan pl;
+    s = ensure_plan(c, d->batch, true, true, pl);  // host_io: the batch's idx / y buffers
+    if (s) return s;
+    s = launch_sample(c, d, D, epoch, it, y_src, pl.idx_dev, pl.y_dev, st);
+    if (s) return s;
+    s = step_grad(c, pl.idx_dev, d->batch, pl.y_dev, grad, 0, pl, st);
+    if (s) return s;
+    if (d->world > 1) {
+      s = dinr_allreduce_grads(c, grad, c->P + 1, stream);
+      if (s) return s;
+    }
+    CUDA_TRY(c, cudaMemcpyAsync(loss + (g - first), grad + c->P, sizeof(float), cudaMemcpyDeviceToDevice, st));
+    s = dinr_adam_step(c, params, grad, m, v, c->P, d->lr0 * std::pow(d->lr_decay, (double)epoch), d->beta1,
+                       d->beta2, d->eps, g + 1, stream);
+    if (s) return s;
+  }
   return DINR_OK;
 }
 

@@ -466,6 +466,7 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
             }
 #pragma unroll
             for (int i = 0; i < 16; ++i) mu_part = fmaf(sWo[col0 + i], hv[i], mu_part);
+#ifdef DINR_F2_PACKED_SUMS
             // column sums over the warp's 32 rows (lanes l and l^16 end with column l & 15): two
             // butterfly levels on packed bf16 pairs, then fp32
             uint32_t hw[8];
@@ -495,6 +496,20 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
                 hv[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
               }
             }
+#else
+            // column sums over the warp's 32 rows in fp32 (lanes l and l^16 end with column l & 15):
+            // four butterfly levels (lane bits 8 .. 1 <-> entries 8 .. 1 apart), then lane bit 16
+#pragma unroll
+            for (int o = 8; o >= 1; o >>= 1) {
+              const bool up = (lane & o) != 0;
+#pragma unroll
+              for (int i = 0; i < o; ++i) {
+                float send = up ? hv[i] : hv[i + o];
+                float keep = up ? hv[i + o] : hv[i];
+                hv[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+              }
+            }
+#endif
             hv[0] += __shfl_xor_sync(0xffffffffu, hv[0], 16);
             if (lane < 16) sHsum[(s * 4 + (warp & 3)) * (H + 4) + col0 + lane] = hv[0];
           }
@@ -636,7 +651,11 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
                 const int cc = hf * 16 + i;
                 const float e0 = top ? 0.5f * u_row * sWo[col0 + cc] : __uint_as_float(v[i]);
                 const float e1 = top ? 0.5f * u_row * sWo[col0 + cc + 1] : __uint_as_float(v[i + 1]);
+#ifdef DINR_F2_PACKED_SUMS
                 dp[c][cc / 2] = bf2_mul(pack_bf16x2(e0, e1), w4[e]);
+#else  // delta = e * swish'(z) in fp32, one bf16 rounding (the MMA operand)
+                dp[c][cc / 2] = pack_bf16x2(e0 * bf16lo(w4[e]), e1 * bf16hi(w4[e]));
+#endif
               }
             }
           }
@@ -662,6 +681,7 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
         if (l >= nu) {  // db of a fused layer: column sums of delta over the warp's 32 rows
 #pragma unroll
           for (int c = 0; c < NCH; ++c) {
+#ifdef DINR_F2_PACKED_SUMS
             // transpose-reduce: the first two butterfly levels on packed bf16 pairs (sums of 2
             // and 4 rows), the last three in fp32; lane l ends with column l's 32-row sum
             uint32_t w[16];
@@ -693,6 +713,26 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
                 d[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
               }
             }
+#else
+            // transpose-reduce in fp32 (five butterfly levels, lane bits 16 .. 1 <-> entries 16 .. 1
+            // apart); lane l ends with column l's 32-row sum
+            float d[32];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              d[2 * i] = bf16lo(dp[c][i]);
+              d[2 * i + 1] = bf16hi(dp[c][i]);
+            }
+#pragma unroll
+            for (int o = 16; o >= 1; o >>= 1) {
+              const bool up = (lane & o) != 0;
+#pragma unroll
+              for (int i = 0; i < o; ++i) {
+                float send = up ? d[i] : d[i + o];
+                float keep = up ? d[i + o] : d[i];
+                d[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+              }
+            }
+#endif
 #pragma unroll
             for (int j = 0; j < 4; ++j)
               if (j == l - nu) dbacc[j][c] += d[0];

@@ -18,6 +18,7 @@ from oracle import oracle as O  # noqa: E402
 n_cases = int(sys.argv[1]) if len(sys.argv) > 1 else 30
 rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 0)
 dev = torch.device("cuda", 0)
+DEEP = os.environ.get("DINR_FUZZ_DEEP") == "1"
 O.lib()
 
 
@@ -27,6 +28,7 @@ def rel(a, b):
 
 
 fails = 0
+ONLY = set(int(x) for x in os.environ.get("DINR_FUZZ_ONLY", "").split(",") if x)
 for k in range(n_cases):
     name = str(rng.choice(["parallel64", "fan512", "cone512", "cone4d512"]))
     over = {}
@@ -35,12 +37,17 @@ for k in range(n_cases):
     if name.startswith("cone"):
         over["sub_z"] = int(rng.choice([1, 2]))
     over["n_s"] = int(rng.choice([32, 64, 128, 256, 512] if name != "parallel64" else [32, 64, 96]))
-    fover = {"C": int(rng.choice([32, 64, 128])), "L": int(rng.integers(1, 8)),
-             "combine": str(rng.choice(["beer", "linear"]))}
+    C_ = int(rng.choice([32, 64, 128]))
+    # depth: within the advertised bf16 envelope (include/dinr.h: L <= 3 / 4 / 6 at H = 64 / 128 / 256,
+    # the BASELINE depths) unless DINR_FUZZ_DEEP=1 draws L in 1..7 at every width
+    lmax = 7 if DEEP else {32: 3, 64: 4, 128: 6}[C_]
+    fover = {"C": C_, "L": int(rng.integers(1, lmax + 1)), "combine": str(rng.choice(["beer", "linear"]))}
     n = int(rng.integers(1, 23))
     prec = "fp32_verify" if rng.random() < 0.2 else "bf16"
     jitter = bool(rng.random() < 0.3)
     gtol, ptol = (1e-4, 1e-5) if prec == "fp32_verify" else (1e-2, 2e-3)
+    if ONLY and k not in ONLY:
+        continue
     g = synth.geometry(name, **over)
     th, t = synth.views(name, **over)
     f = synth.field(name, **fover)
@@ -76,7 +83,8 @@ for k in range(n_cases):
     ok = bool(rc == 0 and ge <= gtol and pe <= ptol and abs(got[P] - ref[P]) <= gtol * abs(ref[P]))
     fails += 0 if ok else 1
     print(json.dumps({"case": k, "ok": ok, "name": name, "over": over, "field": fover, "n": n, "prec": prec, "jitter": jitter,
-                      "path": list(D.train_path(ctx, n)), "grad_err": ge, "proj_err": pe}), flush=True)
+                      "path": list(D.train_path(ctx, n)), "grad_err": ge, "proj_err": pe,
+                      "worst_tensor": int(np.argmax(errs)), "errs": [round(e, 6) for e in errs]}), flush=True)
     D.destroy(ctx)
-print(f"{n_cases - fails}/{n_cases} cases within tolerance")
+print(f"{(len(ONLY) or n_cases) - fails}/{len(ONLY) or n_cases} cases within tolerance")
 sys.exit(1 if fails else 0)
