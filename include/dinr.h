@@ -95,7 +95,14 @@ typedef struct {
 
 /* DINR field network: GRFF with n_freq = C frequencies (width H = 2C), L =
  * n_layers FC(H->H)+Swish layers, FC head H->1 times mu0 (applied once, R6).
- * Supported on the BF16 path: H in {64, 128, 256}; FP32_VERIFY: any H <= 256.
+ * Supported on the BF16 path: H in {64, 128, 256}, 1 <= L <= 64; FP32_VERIFY: any even H <= 256.
+ * Accuracy envelope of the BF16 path (bf16 tensor-core operands, fp32 accumulation and epilogue):
+ * against the fp64 oracle, projections within 2e-3 and gradients within 1e-2 (relative L-inf per
+ * parameter tensor, R23) for L <= 3 at H = 64, L <= 4 at H = 128 and L <= 6 at H = 256
+ * (the BASELINE depths), on inputs whose sums do not cancel (R23b: a bias gradient is a plain sum of
+ * deltas; residuals of both signs that nearly cancel amplify any bf16 error by sum|d| / |sum d|).
+ * Deeper networks run with the error growing with depth (measured 1.5e-2 gradients at H = 64, L = 6).
+ * FP32_VERIFY: projections within 1e-5, gradients within 1e-4.
  * mu0 > 0.  combine: dinr_combine.  precision: dinr_precision. */
 typedef struct {
   int32_t n_freq;

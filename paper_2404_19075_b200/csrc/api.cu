@@ -24,6 +24,9 @@
 #include "k_fused2.cuh"
 #include "k_dw01.cuh"
 #include "k_tc_fwd2.cuh"
+#include "k_tc_bwd2.cuh"
+#include "k_tc_fwd3.cuh"
+#include "k_tc_bwd3.cuh"
 #include "k_infer.cuh"
 #include "k_phantom.cuh"
 #include "k_sampler.cuh"
@@ -244,7 +247,8 @@ size_t plan_layout(dinr_ctx *c, int64_t n, bool train, bool host_io, Plan &pl, v
   } else if (!simt && train) {
     // the split path's training forward runs tiles in pairs (k_tc_fwd2): an even tile count; the
     // padding tile holds only invalid samples, whose upstream factor and so delta are exactly zero
-    pl.n_tiles = 2 * ((pl.nsamp + 255) / 256);
+    // (k_tc_fwd3, H = 256, works in CTA pairs on 4 tiles at a time: a multiple of 4)
+    pl.n_tiles = H == 256 ? 4 * ((pl.nsamp + 511) / 512) : 2 * ((pl.nsamp + 255) / 256);
     pl.hstash = ar.take<uint8_t>((size_t)L * pl.n_tiles * H * 256);
     pl.dstash = ar.take<uint8_t>((size_t)L * pl.n_tiles * H * 256);
     pl.zstash = ar.take<uint8_t>((size_t)L * pl.n_tiles * H * 256);
@@ -354,11 +358,60 @@ dinr_status launch_tc_mlp(dinr_ctx *c, const Plan &pl, int mode, cudaStream_t st
   p.n_tiles = pl.n_tiles;
   p.stash_feat = pl.feat0 ? 0 : 1;
   size_t smem = TcLayout<H>::smem_bytes(c->L, p.resident != 0);
-  if (mode == 2) {
+  if (mode == 2 && H == 256 && std::getenv("DINR_BWD3") && !std::getenv("DINR_BWD2")) {
+    // CTA pairs (cta_group::2, M = 256), two tile streams, W_l blocks double-buffered (k_tc_bwd3.cuh)
+    const size_t sm3 = Bwd3Layout::smem_bytes();
+    dinr_status s = set_smem(c, k_tc_bwd3, sm3);
+    if (s) return s;
+    const int clusters = (int)std::max<int64_t>(1, std::min<int64_t>(pl.n_tiles / 4, c->sm_count / 2));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(2 * clusters), 1, 1);
+    cfg.blockDim = dim3(Bwd3Layout::NT, 1, 1);
+    cfg.dynamicSmemBytes = sm3;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    Launch L_(c, T_BWD, st);
+    CUDA_TRY(c, cudaLaunchKernelEx(&cfg, k_tc_bwd3, p, pl.grid_tc));
+  } else if (mode == 2 && H == 256 && std::getenv("DINR_BWD2")) {
+    // experiment (off by default: measured slower than k_tc_mlp MODE 2, which is HBM-bound, not
+    // weight-load-bound): two tile streams per CTA, W_l streamed in halves shared by both
+    const size_t sm2 = Bwd2Layout::smem_bytes();
+    dinr_status s = set_smem(c, k_tc_bwd2, sm2);
+    if (s) return s;
+    Launch L_(c, T_BWD, st);
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(pl.n_tiles / 2, c->sm_count));
+    k_tc_bwd2<<<grid, Bwd2Layout::NT, sm2, st>>>(p, pl.grid_tc);
+  } else if (mode == 2) {
     dinr_status s = set_smem(c, k_tc_mlp<H, 2>, smem);
     if (s) return s;
     Launch L_(c, T_BWD, st);
     k_tc_mlp<H, 2><<<pl.grid_tc, kTcThreads, smem, st>>>(p);
+  } else if (mode == 1 && H == 256 && !std::getenv("DINR_NO_FWD3") && !std::getenv("DINR_NO_FWD2")) {
+    // CTA pairs (cta_group::2, M = 256), two tile streams, W_l double-buffered (k_tc_fwd3.cuh)
+    const size_t sm3 = Fwd3Layout::smem_bytes(c->L);
+    dinr_status s = set_smem(c, k_tc_fwd3, sm3);
+    if (s) return s;
+    const int clusters = (int)std::max<int64_t>(1, std::min<int64_t>(pl.n_tiles / 4, c->sm_count / 2));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(2 * clusters), 1, 1);
+    cfg.blockDim = dim3(Fwd3Layout::NT, 1, 1);
+    cfg.dynamicSmemBytes = sm3;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    Launch L_(c, T_FWD, st);
+    CUDA_TRY(c, cudaLaunchKernelEx(&cfg, k_tc_fwd3, p));
   } else if (mode == 1 && H == 256 && !std::getenv("DINR_NO_FWD2")) {
     // two tile streams per CTA, W_l streamed in N-halves (k_tc_fwd2.cuh)
     const size_t sm2 = Fwd2Layout::smem_bytes(c->L);

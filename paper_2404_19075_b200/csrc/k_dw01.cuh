@@ -292,7 +292,7 @@ __global__ void __launch_bounds__(Dw01Layout<H>::NT, 1) k_dw01(Dw01Params p) {
         tmem_wait_ld();
 #pragma unroll
         for (int i = 0; i < 8; ++i)
-#ifdef DINR_F2_PACKED_SUMS
+#ifdef DINR_F2_PACKED_DELTA
           hpk[hc][i] = bf2_mul(pack_bf16x2(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1])), s2k[hc][i]);
 #else  // delta_0 = e_0 * swish'(z_0) in fp32, one bf16 rounding (as k_fused2)
           hpk[hc][i] = pack_bf16x2(__uint_as_float(v[2 * i]) * bf16lo(s2k[hc][i]),

@@ -438,7 +438,7 @@ __global__ void __launch_bounds__(FusedLayout<H>::NT, 1) k_fused(FusedParams p) 
                 const int c = hf * 16 + i;
                 float e0 = top ? 0.5f * u_row * sWo[col0 + c] : __uint_as_float(v[i]);
                 float e1 = top ? 0.5f * u_row * sWo[col0 + c + 1] : __uint_as_float(v[i + 1]);
-#ifdef DINR_F2_PACKED_SUMS
+#ifdef DINR_F2_PACKED_DELTA
                 dp[c / 2] = bf2_mul(pack_bf16x2(e0, e1), w4[e]);
 #else  // delta in fp32, one bf16 rounding (as k_fused2)
                 dp[c / 2] = pack_bf16x2(e0 * bf16lo(w4[e]), e1 * bf16hi(w4[e]));

@@ -466,7 +466,7 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
             }
 #pragma unroll
             for (int i = 0; i < 16; ++i) mu_part = fmaf(sWo[col0 + i], hv[i], mu_part);
-#ifdef DINR_F2_PACKED_SUMS
+#ifndef DINR_F2_FP32_SUMS
             // column sums over the warp's 32 rows (lanes l and l^16 end with column l & 15): two
             // butterfly levels on packed bf16 pairs, then fp32
             uint32_t hw[8];
@@ -651,7 +651,7 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
                 const int cc = hf * 16 + i;
                 const float e0 = top ? 0.5f * u_row * sWo[col0 + cc] : __uint_as_float(v[i]);
                 const float e1 = top ? 0.5f * u_row * sWo[col0 + cc + 1] : __uint_as_float(v[i + 1]);
-#ifdef DINR_F2_PACKED_SUMS
+#ifdef DINR_F2_PACKED_DELTA
                 dp[c][cc / 2] = bf2_mul(pack_bf16x2(e0, e1), w4[e]);
 #else  // delta = e * swish'(z) in fp32, one bf16 rounding (the MMA operand)
                 dp[c][cc / 2] = pack_bf16x2(e0 * bf16lo(w4[e]), e1 * bf16hi(w4[e]));
@@ -681,7 +681,7 @@ __global__ void __launch_bounds__(Fused2Layout<H>::NT, 1) k_fused2(FusedParams p
         if (l >= nu) {  // db of a fused layer: column sums of delta over the warp's 32 rows
 #pragma unroll
           for (int c = 0; c < NCH; ++c) {
-#ifdef DINR_F2_PACKED_SUMS
+#ifndef DINR_F2_FP32_SUMS
             // transpose-reduce: the first two butterfly levels on packed bf16 pairs (sums of 2
             // and 4 rows), the last three in fp32; lane l ends with column l's 32-row sum
             uint32_t w[16];

@@ -1,6 +1,6 @@
 """Randomized gradient/projection parity sweep against the fp64 oracle (test infrastructure; run
 by hand: python tests/_fuzz_parity.py [n_cases] [seed]).  Draws beams, sub-ray layouts, N_s, widths,
-depths, combines and ragged batch sizes, and checks the training step's gradient (1e-2) and the
+depths, combines and ragged batch sizes on conditioned inputs (see below), and checks the training step's gradient (1e-2) and the
 projection (2e-3) per case.  Prints one line per case and a summary; exit code 1 on any failure."""
 import json
 import os
@@ -19,7 +19,10 @@ n_cases = int(sys.argv[1]) if len(sys.argv) > 1 else 30
 rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 0)
 dev = torch.device("cuda", 0)
 DEEP = os.environ.get("DINR_FUZZ_DEEP") == "1"
+PHANTOM_Y = os.environ.get("DINR_FUZZ_PHANTOM_Y") == "1"
 O.lib()
+if os.environ.get("DINR_LIB"):  # a variant build (python -m paper_2404_19075_b200.build --variant ...)
+    D.load(os.path.join(ROOT, "paper_2404_19075_b200", os.environ["DINR_LIB"]))
 
 
 def rel(a, b):
@@ -52,7 +55,11 @@ for k in range(n_cases):
     th, t = synth.views(name, **over)
     f = synth.field(name, **fover)
     B = synth.grff_matrix(f["C"], f["sigma_t"], f["sigma_s"], seed=1 + k)
-    prm = synth.init_params(f["C"], f["L"], seed=2 + k)
+    # conditioned inputs (default; R23): a positive head bias, so that the attenuation
+    # mu = mu0 (w_o . h + b_o) is mostly >= 0 as a LAC is (no cancellation along a ray), and
+    # measured data above the model (y - f_hat > 0 for every pixel: no cancellation across pixels in
+    # the bias gradients).  DINR_FUZZ_PHANTOM_Y=1: default init and the phantom's exact projections.
+    prm = synth.init_params(f["C"], f["L"], seed=2 + k, head_bias=None if PHANTOM_Y else 0.5)
     ctx = D.create(0)
     D.set_geometry(ctx, g, th, t)
     D.set_field_weights(ctx, f, torch.tensor(B, device=dev), torch.tensor(prm, device=dev), precision=prec)
@@ -60,7 +67,11 @@ for k in range(n_cases):
         D.set_sampling(ctx, "jitter", 1234 + k, 7)
         g = dict(g, sampling="jitter", seed=1234 + k, step=7)
     idx = synth.pixel_batch(name, n, seed=100 + k, **over)
-    y, _, _ = O.project_exact(g, th, t, synth.phantom(name), idx, f["combine"])
+    rf, _, _ = O.project(g, th, t, f, B, prm, idx)
+    if PHANTOM_Y:
+        y, _, _ = O.project_exact(g, th, t, synth.phantom(name), idx, f["combine"])
+    else:
+        y = rf + np.random.default_rng(300 + k).uniform(0.05, 0.5, n) * max(np.max(np.abs(rf)), 1e-3)
     y = y.astype(np.float32)
     P = synth.param_count(f["C"], f["L"])
     grad = torch.zeros(P + 1, device=dev)
@@ -69,7 +80,6 @@ for k in range(n_cases):
     D.project(ctx, torch.tensor(idx, device=dev), fhat)
     torch.cuda.synchronize()
     ref, rc = O.project_and_grad(g, th, t, f, B, prm, idx, y)
-    rf, _, _ = O.project(g, th, t, f, B, prm, idx)
     got = grad.cpu().numpy()
     H, off, errs = 2 * f["C"], 0, []
     for _ in range(f["L"]):
