@@ -19,6 +19,7 @@
 #include "k_simt.cuh"
 #include "k_small.cuh"
 #include "k_tc_dw.cuh"
+#include "k_tc_dwz.cuh"
 #include "k_tc_mlp.cuh"
 #include "k_fused.cuh"
 #include "k_fused2.cuh"
@@ -110,6 +111,7 @@ struct Plan {
   bool fused, fused2;  // fused2: two concurrent tile streams (k_fused2)
   bool dw01;           // layers 0 and 1 unfused, both inputs recomputed by k_dw01 (no input stash)
   bool feat0;          // the dW GEMM recomputes layer 0's input (needs N_s a power of two)
+  bool zall;           // H = 256 split path: y = z/2 stash only; K3 / the dW GEMM recompute swish', h
   int nf, nu, grid_f, dw_layers;
   uint8_t *ring;
   float *dwf, *dbf;
@@ -118,6 +120,7 @@ struct Plan {
   uint2 *rid;   // global ray ids (N3 keys)
   Jitter jit;   // N3 sample placement handed to the MLP kernels
   float *pchunk, *u, *fhat, *loss_part, *head_part, *dw_part, *db_part, *colsum;
+  float *db3;  // zall: K3's per-CTA bias-gradient partials [L][2][grid_tc][128]
   float *wq;  // per-ray quadrature weight (K1 -> K4)
   uint8_t *hstash, *dstash, *zstash;
   float *sh, *sz, *sd;
@@ -148,6 +151,12 @@ bool use_fused(const dinr_ctx *c) {
 bool use_fused2(const dinr_ctx *c) {
   static const bool off = std::getenv("DINR_FUSED_V1") != nullptr;
   return fused2_fits(c) && !(off && fused1_fits(c));
+}
+
+// the H = 256 split path's K2 on CTA pairs (k_tc_fwd3), with the y-only stash (zall)
+bool fwd3_on() {
+  static const bool off = std::getenv("DINR_NO_FWD3") != nullptr || std::getenv("DINR_NO_FWD2") != nullptr;
+  return !off;
 }
 
 int loss_blocks_for(int64_t n) { return (int)std::max<int64_t>(1, (n + kLossThreads - 1) / kLossThreads); }
@@ -187,6 +196,13 @@ size_t plan_layout(dinr_ctx *c, int64_t n, bool train, bool host_io, Plan &pl, v
   pl.fhat = ar.take<float>(n + 1);
   pl.loss_part = ar.take<float>(pl.nloss + 1);
   const bool simt = c->field.precision == DINR_FP32_VERIFY;
+  // H = 256 split path with k_tc_fwd3 (y-only stash): the dW GEMM k_tc_dwz runs one CTA per
+  // (layer, K-split) for both output blocks
+  // (experiment, off by default: measured no faster -- the forward saves its writes but K3 and the
+  // dW GEMM redo the MUFU work)
+  static const bool zall_on = std::getenv("DINR_ZALL") != nullptr;
+  const bool zall_path = train && !simt && !use_fused(c) && c->H == 256 && fwd3_on() && zall_on;
+  if (zall_path) pl.ks0 = pl.ks1 = pl.ksplit = (int)std::max<int64_t>(1, std::min<int64_t>(pl.n_tiles, c->sm_count / c->L));
   const int ks = simt ? pl.ksplit_simt : pl.ksplit;
   pl.head_part = ar.take<float>((size_t)std::max(pl.grid_tc, ks) * (H + 1));
   pl.dw_part = pl.db_part = nullptr;
@@ -202,6 +218,8 @@ size_t plan_layout(dinr_ctx *c, int64_t n, bool train, bool host_io, Plan &pl, v
   // layer 0's features recomputed by the dW GEMM instead of stashed: on the fused path (for the
   // split path, H = 256, the recompute of 128 frequencies costs more than the stash traffic)
   pl.feat0 = pl.fused;
+  pl.zall = false;
+  pl.db3 = nullptr;
   pl.nf = pl.nu = pl.grid_f = 0;
   pl.dw_layers = L;
   pl.ring = nullptr;
@@ -249,7 +267,11 @@ size_t plan_layout(dinr_ctx *c, int64_t n, bool train, bool host_io, Plan &pl, v
     // padding tile holds only invalid samples, whose upstream factor and so delta are exactly zero
     // (k_tc_fwd3, H = 256, works in CTA pairs on 4 tiles at a time: a multiple of 4)
     pl.n_tiles = H == 256 ? 4 * ((pl.nsamp + 511) / 512) : 2 * ((pl.nsamp + 255) / 256);
-    pl.hstash = ar.take<uint8_t>((size_t)L * pl.n_tiles * H * 256);
+    // H = 256 with k_tc_fwd3: the forward stashes y = z / 2 of every layer (fp16) and nothing else
+    pl.zall = zall_path;
+    pl.feat0 = pl.zall;
+    if (!pl.zall) pl.hstash = ar.take<uint8_t>((size_t)L * pl.n_tiles * H * 256);
+    if (pl.zall) pl.db3 = ar.take<float>((size_t)L * 2 * pl.grid_tc * 128);
     pl.dstash = ar.take<uint8_t>((size_t)L * pl.n_tiles * H * 256);
     pl.zstash = ar.take<uint8_t>((size_t)L * pl.n_tiles * H * 256);
   }
@@ -357,8 +379,10 @@ dinr_status launch_tc_mlp(dinr_ctx *c, const Plan &pl, int mode, cudaStream_t st
   p.head_part = pl.head_part;
   p.n_tiles = pl.n_tiles;
   p.stash_feat = pl.feat0 ? 0 : 1;
+  p.zall = pl.zall ? 1 : 0;
+  p.db3 = pl.db3;
   size_t smem = TcLayout<H>::smem_bytes(c->L, p.resident != 0);
-  if (mode == 2 && H == 256 && std::getenv("DINR_BWD3") && !std::getenv("DINR_BWD2")) {
+  if (mode == 2 && H == 256 && !pl.zall && std::getenv("DINR_BWD3") && !std::getenv("DINR_BWD2")) {
     // CTA pairs (cta_group::2, M = 256), two tile streams, W_l blocks double-buffered (k_tc_bwd3.cuh)
     const size_t sm3 = Bwd3Layout::smem_bytes();
     dinr_status s = set_smem(c, k_tc_bwd3, sm3);
@@ -378,7 +402,7 @@ dinr_status launch_tc_mlp(dinr_ctx *c, const Plan &pl, int mode, cudaStream_t st
     cfg.numAttrs = 1;
     Launch L_(c, T_BWD, st);
     CUDA_TRY(c, cudaLaunchKernelEx(&cfg, k_tc_bwd3, p, pl.grid_tc));
-  } else if (mode == 2 && H == 256 && std::getenv("DINR_BWD2")) {
+  } else if (mode == 2 && H == 256 && !pl.zall && std::getenv("DINR_BWD2")) {
     // experiment (off by default: measured slower than k_tc_mlp MODE 2, which is HBM-bound, not
     // weight-load-bound): two tile streams per CTA, W_l streamed in halves shared by both
     const size_t sm2 = Bwd2Layout::smem_bytes();
@@ -387,12 +411,17 @@ dinr_status launch_tc_mlp(dinr_ctx *c, const Plan &pl, int mode, cudaStream_t st
     Launch L_(c, T_BWD, st);
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(pl.n_tiles / 2, c->sm_count));
     k_tc_bwd2<<<grid, Bwd2Layout::NT, sm2, st>>>(p, pl.grid_tc);
+  } else if (mode == 2 && pl.zall) {
+    dinr_status s = set_smem(c, k_tc_mlp<H, 3>, smem);
+    if (s) return s;
+    Launch L_(c, T_BWD, st);
+    k_tc_mlp<H, 3><<<pl.grid_tc, kTcThreads, smem, st>>>(p);
   } else if (mode == 2) {
     dinr_status s = set_smem(c, k_tc_mlp<H, 2>, smem);
     if (s) return s;
     Launch L_(c, T_BWD, st);
     k_tc_mlp<H, 2><<<pl.grid_tc, kTcThreads, smem, st>>>(p);
-  } else if (mode == 1 && H == 256 && !std::getenv("DINR_NO_FWD3") && !std::getenv("DINR_NO_FWD2")) {
+  } else if (mode == 1 && H == 256 && fwd3_on()) {
     // CTA pairs (cta_group::2, M = 256), two tile streams, W_l double-buffered (k_tc_fwd3.cuh)
     const size_t sm3 = Fwd3Layout::smem_bytes(c->L);
     dinr_status s = set_smem(c, k_tc_fwd3, sm3);
@@ -410,8 +439,32 @@ dinr_status launch_tc_mlp(dinr_ctx *c, const Plan &pl, int mode, cudaStream_t st
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    Launch L_(c, T_FWD, st);
-    CUDA_TRY(c, cudaLaunchKernelEx(&cfg, k_tc_fwd3, p));
+#ifdef DINR_PHASES
+    static unsigned long long *dbg3 = nullptr;
+    if (!dbg3) cudaMalloc(&dbg3, sizeof(unsigned long long) * 32 * 1024);
+    cudaMemsetAsync(dbg3, 0, sizeof(unsigned long long) * 32 * 1024, st);
+    p.dbg = dbg3;
+#endif
+    {
+      Launch L_(c, T_FWD, st);
+      CUDA_TRY(c, cudaLaunchKernelEx(&cfg, k_tc_fwd3, p));
+    }
+#ifdef DINR_PHASES
+    {
+      std::vector<unsigned long long> h((size_t)2 * clusters * 32);
+      cudaStreamSynchronize(st);
+      cudaMemcpy(h.data(), dbg3, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost);
+      double tot[16] = {0};
+      for (int b = 0; b < 2 * clusters; ++b)
+        for (int k = 0; k < 16; ++k) tot[k] += (double)h[(size_t)b * 32 + k];
+      const double it = (double)(pl.n_tiles / 4) * 2.0;  // CTA-iterations (both CTAs of every cluster)
+      std::fprintf(stderr, "[fwd3 phases] cycles per CTA-iteration: s0 feat %.0f accwait %.0f epi %.0f | s1 feat %.0f "
+                           "accwait %.0f epi %.0f | mma wait_w %.0f wait_a %.0f | loader wait_free %.0f wait_own %.0f | "
+                           "store wait_a %.0f wait_read %.0f\n",
+                   tot[0] / it, tot[1] / it, tot[2] / it, tot[4] / it, tot[5] / it, tot[6] / it, 2 * tot[8] / it,
+                   2 * tot[9] / it, tot[10] / it, 2 * tot[11] / it, tot[12] / it, tot[13] / it);
+    }
+#endif
   } else if (mode == 1 && H == 256 && !std::getenv("DINR_NO_FWD2")) {
     // two tile streams per CTA, W_l streamed in N-halves (k_tc_fwd2.cuh)
     const size_t sm2 = Fwd2Layout::smem_bytes(c->L);
@@ -448,18 +501,28 @@ dinr_status launch_tc_dw(dinr_ctx *c, const Plan &pl, cudaStream_t st) {
   p.dw_part = pl.dw_part;
   p.db_part = pl.db_part;
   p.feat0 = pl.feat0 ? 1 : 0;  // layer 0's input (GRFF features) recomputed, not stashed
+  p.ystash = pl.zstash;  // k_tc_dwz: inputs of layers >= 1 rebuilt from the y stash
   p.rec32 = pl.rec32;
   p.B = c->d_B;
   p.n_s = c->geom.samples_per_ray;
   p.lg_ns = 0;
   while ((1 << p.lg_ns) < p.n_s) ++p.lg_ns;
   p.nsamp = pl.nsamp;
+  p.ks0 = pl.ks0;
+  p.ks1 = pl.ks1;
+  if (H == 256 && pl.zall) {
+    const size_t smz = DwzLayout::smem_bytes();
+    dinr_status s = set_smem(c, k_tc_dwz, smz);
+    if (s) return s;
+    Launch L_(c, T_DW, st);
+    k_tc_dwz<<<dim3(pl.dw_layers * pl.ks1, 1, 1), DwzLayout::NT, smz, st>>>(p);
+    CUDA_TRY(c, cudaGetLastError());
+    return DINR_OK;
+  }
   size_t smem = DwLayout<H>::smem_bytes();
   dinr_status s = set_smem(c, k_tc_dw<H>, smem);
   if (s) return s;
   Launch L_(c, T_DW, st);
-  p.ks0 = pl.ks0;
-  p.ks1 = pl.ks1;
   k_tc_dw<H><<<dim3(pl.ks0 + (pl.dw_layers - 1) * pl.ks1, pl.nmb, 1), DwLayout<H>::NT, smem, st>>>(p);
   CUDA_TRY(c, cudaGetLastError());
   return DINR_OK;
@@ -769,9 +832,9 @@ dinr_status step_grad(dinr_ctx *c, const int64_t *idx, int64_t n, const float *y
   if (s) return s;
   {
     Launch L_(c, T_ASM, st);
-    k_assemble<<<(unsigned)((c->P + 1 + 255) / 256), 256, 0, st>>>(c->H, c->L, c->P, pl.nmb, ks, pl.dw_part,
-                                                                   pl.db_part, pl.head_part, nhead, pl.loss_part,
-                                                                   pl.nloss, 1.f / (float)n, accumulate, grad);
+    k_assemble<<<(unsigned)((c->P + 1 + 255) / 256), 256, 0, st>>>(
+        c->H, c->L, c->P, pl.nmb, ks, pl.dw_part, pl.zall ? pl.db3 : pl.db_part, pl.zall ? pl.grid_tc : ks,
+        pl.head_part, nhead, pl.loss_part, pl.nloss, 1.f / (float)n, accumulate, grad);
   }
   CUDA_TRY(c, cudaGetLastError());
   return DINR_OK;

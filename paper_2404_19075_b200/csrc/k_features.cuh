@@ -15,8 +15,10 @@ __device__ __forceinline__ float4 grff_coords(const float4 *__restrict__ rec32, 
                                               bool valid, const Jitter &jt) {
   float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
   if (valid) {
-    const int64_t ray = g >> lg_ns;
-    const uint32_t j = (uint32_t)(g & (n_s - 1));
+    // N_s a power of two: shifts; otherwise (split path, e.g. N_s = 96) a division
+    const int64_t ray = (n_s & (n_s - 1)) == 0 ? g >> lg_ns
+                        : ((g >> 32) == 0 ? (int64_t)((uint32_t)g / (uint32_t)n_s) : g / n_s);
+    const uint32_t j = (uint32_t)(g - ray * n_s);
     const float jj = (float)j + sample_offset(jt, ray, j);  // midpoint (R8) or N3 jitter
     const float4 ra = rec32[2 * ray], rv = rec32[2 * ray + 1];
     r.x = ra.w;

@@ -102,8 +102,10 @@ __global__ void __launch_bounds__(kLossThreads) k_loss(const float *__restrict__
 // dw_part layout: [L][nmb][ksplit][128][H]; db_part: [L][nmb][ksplit][128];
 // head_part: [nhead][H+1].
 // ---------------------------------------------------------------------------------------
+// db_part uses the split count ks_db (the zall path's bias partials come from K3's CTAs, the
+// weight partials from the dW GEMM's K-split).
 __global__ void k_assemble(int H, int L, int64_t P, int nmb, int ksplit, const float *__restrict__ dw_part,
-                           const float *__restrict__ db_part, const float *__restrict__ head_part, int nhead,
+                           const float *__restrict__ db_part, int ks_db, const float *__restrict__ head_part, int nhead,
                            const float *__restrict__ loss_part, int nloss, float inv_n, int accumulate,
                            float *__restrict__ grad) {
   int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -124,8 +126,8 @@ __global__ void k_assemble(int H, int L, int64_t P, int nmb, int ksplit, const f
     } else {
       int o = (int)(e - (int64_t)H * H);
       int mb = o >> 7, ol = o & 127;
-      const float *src = db_part + (((int64_t)l * nmb + mb) * ksplit) * 128 + ol;
-      for (int s = 0; s < ksplit; ++s) v += src[(int64_t)s * 128];
+      const float *src = db_part + (((int64_t)l * nmb + mb) * ks_db) * 128 + ol;
+      for (int s = 0; s < ks_db; ++s) v += src[(int64_t)s * 128];
     }
   } else {
     int k = (int)(q - (int64_t)L * per);  // 0..H-1 -> w_o, H -> b_o

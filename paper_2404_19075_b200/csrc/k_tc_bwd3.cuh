@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(Bwd3Layout::NT, 1) k_tc_bwd3(TcParams p, int n
         for (int s = 0; s < 2; ++s) {
           for (int h = 0; h < 2; ++h, ++step) {
             const uint32_t b = step & 1;
-            if (step >= 2) mbar_wait_cluster(&w_free[b], ((step >> 1) - 1) & 1);
+            if (step >= 2) mbar_wait(&w_free[b], ((step >> 1) - 1) & 1);
             uint64_t *bar = leader ? &w_full[b] : &w_loc[b];
             mbar_arrive_expect_tx(bar, WQ);
             // this CTA's 64-column block 2h + r of the MN-major W_l image (input features)
@@ -189,7 +189,7 @@ __global__ void __launch_bounds__(Bwd3Layout::NT, 1) k_tc_bwd3(TcParams p, int n
         uint4 zt[2][2];
         ld_global_v8_hint(zsrc + (size_t)(cb_lo * 2) * 128 * 32, zt[0][0], zt[0][1], pol_z);
         if (a_busy) {
-          mbar_wait_cluster(&acc_full[s], accph);
+          mbar_wait(&acc_full[s], accph);  // CTA scope: TMEM + own smem only
           accph ^= 1;
         }
         a_busy = true;
@@ -253,7 +253,7 @@ __global__ void __launch_bounds__(Bwd3Layout::NT, 1) k_tc_bwd3(TcParams p, int n
         if (l >= 2 && cg == 0 && (row & 31) == 0)  // the next step's state into L2 meanwhile
           bulk_prefetch_l2(p.zstash + ((size_t)(l - 2) * p.n_tiles + tile) * kZTile + (size_t)(row >> 5) * (kZTile / 4),
                            kZTile / 4);
-        mbar_wait_cluster(&acc_full[s], accph);
+        mbar_wait(&acc_full[s], accph);  // CTA scope: TMEM + own smem only
         accph ^= 1;
         tc_fence_after();
 #pragma unroll
@@ -282,7 +282,7 @@ __global__ void __launch_bounds__(Bwd3Layout::NT, 1) k_tc_bwd3(TcParams p, int n
       }
     }
     if (a_busy) {  // the last delta_0 store has read A_s
-      mbar_wait_cluster(&acc_full[s], accph);
+      mbar_wait(&acc_full[s], accph);  // CTA scope: TMEM + own smem only
       accph ^= 1;
     }
   }

@@ -29,12 +29,17 @@ struct DwParams {
   int n_s, lg_ns;
   int64_t nsamp;
   Jitter jit;
+  // k_tc_dwz (H = 256 split path with k_tc_fwd3): layer inputs h_l (l >= 1) rebuilt from the
+  // forward's fp16 y = z / 2 stash
+  const uint8_t *ystash;
 };
 
 // The tensor core's fp32 accumulation loses precision with the length of the chain of MMAs into
 // one TMEM accumulator (measured: the cone512 gradient's deviation from batch linearity grew in
-// proportion to the tiles per CTA, 1.3e-3 at 2730 tiles).  Non-feature CTAs therefore restart the
-// accumulator every kDwFlushTiles tiles and warps 2-9 add it into fp32 registers.
+// proportion to the tiles per CTA, 1.3e-3 at 2730 tiles).  Every CTA therefore restarts the
+// accumulator every kDwFlushTiles tiles and warps 2-9 add it into fp32 registers (in CTAs whose B
+// operand is computed on chip -- layer-0 features, or h from the y stash -- the same warps build it,
+// the flushes interleaved with the tiles).
 constexpr int kDwFlushTiles = 64;
 
 template <int H>
@@ -69,7 +74,7 @@ __global__ void __launch_bounds__(DwLayout<H>::NT, 1) k_tc_dw(DwParams p) {
   const int split = bx < p.ks0 ? bx : (bx - p.ks0) % p.ks1;
   const int ks = l == 0 ? p.ks0 : p.ks1;
   const bool feat = p.feat0 && l == 0;
-  const bool fl = !feat;  // chunked accumulation (warps 2-9 are free to flush)
+  const bool fl = true;  // chunked accumulation (warps 2-9 flush every kDwFlushTiles tiles)
   if (warp == 0) {
     tmem_alloc(tmem_slot, LY::TMEM_COLS);
     tmem_relinquish();
@@ -140,30 +145,6 @@ __global__ void __launch_bounds__(DwLayout<H>::NT, 1) k_tc_dw(DwParams p) {
       if (fl && (ci == kDwFlushTiles - 1 || it == count - 1)) umma_commit(flush_full);
     }
     umma_commit(done);
-  } else if (warp >= 2 && feat) {
-    // B operand of layer 0 = gamma(x) of the tile's 128 samples, same SW128 image the fused
-    // kernel fed to its layer-0 MMA (thread = sample row)
-    const int row = ((warp & 3) << 5) | (tid & 31);
-    const int half = (warp - 2) >> 2;  // frequencies [half C/2, (half + 1) C/2)
-    constexpr int C = H / 2;
-    int it = 0;
-    for (int64_t t = split; t < p.n_tiles; t += ks, ++it) {
-      const int st = it % NST;
-      const int64_t g = t * 128 + row;
-      const float4 rb = grff_coords(p.rec32, g, p.lg_ns, p.n_s, g < p.nsamp, p.jit);
-      if (it >= NST) mbar_wait(&empty[st], ((it / NST) - 1) & 1);
-      const uint32_t sb = smem_u32(smem + st * LY::STAGE + LY::A_STAGE);
-#pragma unroll
-      for (int c0 = half * (C / 2); c0 < (half + 1) * (C / 2); c0 += 8) {
-        uint32_t pc[4], ps[4];
-        grff8(sB4, c0, rb, pc, ps);
-        st_shared_v4(sb + sw128_offset(row, c0, 128), pc[0], pc[1], pc[2], pc[3]);
-        st_shared_v4(sb + sw128_offset(row, C + c0, 128), ps[0], ps[1], ps[2], ps[3]);
-      }
-      fence_proxy_async_smem();
-      __syncwarp();
-      if ((tid & 31) == 0) mbar_arrive(&full[st]);
-    }
   }
   if (fl && warp >= 2 && warp < 10) {
     // flush warps: thread = (accumulator lane o, column half cp); every chunk of kDwFlushTiles
@@ -174,7 +155,55 @@ __global__ void __launch_bounds__(DwLayout<H>::NT, 1) k_tc_dw(DwParams p) {
 #pragma unroll
     for (int i = 0; i < H / 2; ++i) racc[i] = 0.f;
     const int nch = (count + kDwFlushTiles - 1) / kDwFlushTiles;
-    for (int c = 0; c < nch; ++c) {
+    int c0 = 0;
+    if (feat) {
+      // layer 0's B operand built on chip, interleaved with the accumulator flushes: chunk c is
+      // flushed before the tile that would need the stage its restart holds back
+      int it = 0;
+      for (int64_t t = split; t < p.n_tiles; t += ks, ++it) {
+        while (c0 < nch && c0 * kDwFlushTiles + kDwFlushTiles - 1 <= it - NST) {
+          mbar_wait(flush_full, c0 & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int cb = 0; cb < H / 64; ++cb) {
+            uint32_t v[32];
+            tmem_ld32(tmem_dw + trow + cp * (H / 2) + cb * 32, v);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) racc[cb * 32 + i] += __uint_as_float(v[i]);
+          }
+          if (cp == 0) {
+            uint32_t v[16];
+            tmem_ld16(tmem_db + trow, v);
+            tmem_wait_ld();
+            rdb += __uint_as_float(v[0]);
+          }
+          tc_fence_before();
+          __syncwarp();
+          if ((tid & 31) == 0) mbar_arrive(flush_free);
+          ++c0;
+        }
+        const int st = it % NST;
+        const uint32_t sb = smem_u32(smem + st * LY::STAGE + LY::A_STAGE);
+        // layer 0: B = gamma(x) of the tile's 128 samples, the same SW128 image the forward fed to
+        // its layer-0 MMA (thread = sample row o, frequency half cp)
+        constexpr int C = H / 2;
+        const int64_t g = t * 128 + o;
+        const float4 rb = grff_coords(p.rec32, g, p.lg_ns, p.n_s, g < p.nsamp, p.jit);
+        if (it >= NST) mbar_wait(&empty[st], ((it / NST) - 1) & 1);
+#pragma unroll
+        for (int f0 = cp * (C / 2); f0 < (cp + 1) * (C / 2); f0 += 8) {
+          uint32_t pc[4], ps[4];
+          grff8(sB4, f0, rb, pc, ps);
+          st_shared_v4(sb + sw128_offset(o, f0, 128), pc[0], pc[1], pc[2], pc[3]);
+          st_shared_v4(sb + sw128_offset(o, C + f0, 128), ps[0], ps[1], ps[2], ps[3]);
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if ((tid & 31) == 0) mbar_arrive(&full[st]);
+      }
+    }
+    for (int c = c0; c < nch; ++c) {
       mbar_wait(flush_full, c & 1);
       tc_fence_after();
 #pragma unroll
@@ -214,41 +243,6 @@ __global__ void __launch_bounds__(DwLayout<H>::NT, 1) k_tc_dw(DwParams p) {
   if (count > 0) {
     mbar_wait(done, 0);
     tc_fence_after();
-  }
-  // epilogue of feature CTAs (warps 2-5): lane o of the accumulator -> fp32 partial row
-  if (!fl && warp >= 2 && warp < 6) {
-    const int o = ((warp & 3) << 5) | (tid & 31);
-    const uint32_t trow = (uint32_t)((warp & 3) * 32) << 16;
-    float *dst = p.dw_part + ((((size_t)l * p.nmb + mb) * p.ksplit + split) * 128 + o) * H;
-    const bool live = (H >= 128) || o < 64;
-#pragma unroll 1
-    for (int cb = 0; cb < H / 32; ++cb) {
-      uint32_t v[32];
-      tmem_ld32(tmem_dw + trow + cb * 32, v);
-      tmem_wait_ld();
-      if (live) {
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          float4 f = count > 0 ? make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
-                                             __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3]))
-                               : make_float4(0.f, 0.f, 0.f, 0.f);
-          reinterpret_cast<float4 *>(dst + cb * 32)[q] = f;
-        }
-      }
-    }
-    {
-      uint32_t v[16];
-      tmem_ld16(tmem_db + trow, v);
-      tmem_wait_ld();
-      if (live) p.db_part[(((size_t)l * p.nmb + mb) * p.ksplit + split) * 128 + o] = count > 0 ? __uint_as_float(v[0]) : 0.f;
-    }
-    // slots this layer does not use (ks < ksplit) are zero for the fixed-order reduction
-    if (live)
-      for (int s2 = split + ks; s2 < p.ksplit; s2 += ks) {
-        float4 *z = reinterpret_cast<float4 *>(p.dw_part + ((((size_t)l * p.nmb + mb) * p.ksplit + s2) * 128 + o) * H);
-        for (int q = 0; q < H / 4; ++q) z[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-        p.db_part[(((size_t)l * p.nmb + mb) * p.ksplit + s2) * 128 + o] = 0.f;
-      }
   }
   tc_fence_before();
   __syncthreads();

@@ -36,6 +36,14 @@
 
 namespace dinr {
 
+#ifdef DINR_PHASES
+#define F3_T0() const long long _t0 = clock64()
+#define F3_ACC(v) (v) += (unsigned long long)(clock64() - _t0)
+#else
+#define F3_T0() (void)0
+#define F3_ACC(v) (void)0
+#endif
+
 struct Fwd3Layout {
   static constexpr int H = 256, C = 128;
   static constexpr int NT = 512 + 96;
@@ -79,7 +87,9 @@ __global__ void __launch_bounds__(Fwd3Layout::NT, 1) k_tc_fwd3(TcParams p) {
     fence_mbar_init();
   }
   const int64_t per = (int64_t)H * H + H;
-  for (int i = tid; i < L * H; i += LY::NT) sBias[i] = p.params[(i / H) * per + (int64_t)H * H + (i % H)];
+  // zall: the epilogue works on y = z / 2 = 0.5 acc + 0.5 b (one FFMA), so the bias is stored halved
+  const float bscale = p.zall ? 0.5f : 1.f;
+  for (int i = tid; i < L * H; i += LY::NT) sBias[i] = bscale * p.params[(i / H) * per + (int64_t)H * H + (i % H)];
   for (int i = tid; i <= H; i += LY::NT) sWo[i] = p.params[(int64_t)L * per + i];
   for (int i = tid; i < C * 4; i += LY::NT) sB[i] = p.B[i];
   cluster_sync();  // barriers of both CTAs initialized before any remote arrive
@@ -101,14 +111,21 @@ __global__ void __launch_bounds__(Fwd3Layout::NT, 1) k_tc_fwd3(TcParams p) {
       const uint32_t idesc = idesc_bf16(256, 128, 0, 0);
       uint32_t aph[2] = {0, 0};
       uint32_t step = 0;
+      [[maybe_unused]] unsigned long long ph_w = 0, ph_a = 0;
       for (int64_t pi = cl; pi < n_iter; pi += ncl) {
         for (int l = 0; l < L; ++l) {
           for (int s = 0; s < 2; ++s) {
             for (int h = 0; h < 2; ++h, ++step) {
               const uint32_t b = step & 1;
-              mbar_wait_cluster(&w_full[b], (step >> 1) & 1);
+              {
+                F3_T0();
+                mbar_wait_cluster(&w_full[b], (step >> 1) & 1);
+                F3_ACC(ph_w);
+              }
               if (h == 0) {
+                F3_T0();
                 mbar_wait_cluster(&a_full[s], aph[s]);
+                F3_ACC(ph_a);
                 aph[s] ^= 1;
               }
               tc_fence_after();
@@ -125,18 +142,29 @@ __global__ void __launch_bounds__(Fwd3Layout::NT, 1) k_tc_fwd3(TcParams p) {
           }
         }
       }
+#ifdef DINR_PHASES
+      if (p.dbg) {
+        p.dbg[(size_t)blockIdx.x * 32 + 8] = ph_w;
+        p.dbg[(size_t)blockIdx.x * 32 + 9] = ph_a;
+      }
+#endif
     }
   } else if (tid == 544) {
     // ============================================================ W loads (both CTAs)
     const uint8_t *wsrc = reinterpret_cast<const uint8_t *>(p.wpack);
     const uint32_t w_full_leader = mapa_shared(smem_u32(&w_full[0]), 0);
     uint32_t step = 0;
+    [[maybe_unused]] unsigned long long ph_lf = 0, ph_ll = 0;
     for (int64_t pi = cl; pi < n_iter; pi += ncl) {
       for (int l = 0; l < L; ++l) {
         for (int s = 0; s < 2; ++s) {
           for (int h = 0; h < 2; ++h, ++step) {
             const uint32_t b = step & 1;
-            if (step >= 2) mbar_wait_cluster(&w_free[b], ((step >> 1) - 1) & 1);
+            if (step >= 2) {
+              F3_T0();
+              mbar_wait(&w_free[b], ((step >> 1) - 1) & 1);
+              F3_ACC(ph_lf);
+            }
             uint64_t *bar = leader ? &w_full[b] : &w_loc[b];
             mbar_arrive_expect_tx(bar, WQ);
             // this CTA's rows [128 h + 64 r, +64) of every 64-column K-block of the W_l image
@@ -144,33 +172,54 @@ __global__ void __launch_bounds__(Fwd3Layout::NT, 1) k_tc_fwd3(TcParams p) {
               bulk_g2s(sW + b * WQ + kb * 8192, wsrc + (size_t)l * W_LAYER + kb * (H * 128) + (size_t)(128 * h + 64 * rank) * 128,
                        8192, bar);
             if (!leader) {
+              F3_T0();
               mbar_wait(&w_loc[b], (step >> 1) & 1);
+              F3_ACC(ph_ll);
               mbar_arrive_remote(w_full_leader + b * 8);
             }
           }
         }
       }
     }
+#ifdef DINR_PHASES
+    if (p.dbg) {
+      p.dbg[(size_t)blockIdx.x * 32 + 10] = ph_lf;
+      p.dbg[(size_t)blockIdx.x * 32 + 11] = ph_ll;
+    }
+#endif
   } else if (tid == 576) {
     // ============================================================ h-stash stores (both CTAs)
     uint32_t rph[2] = {0, 0};
+    [[maybe_unused]] unsigned long long ph_sa = 0, ph_sr = 0;
     for (int64_t pi = cl; pi < n_iter; pi += ncl) {
       for (int l = 0; l < L; ++l) {
         for (int s = 0; s < 2; ++s) {
-          mbar_wait(&a_rdy[s], rph[s]);
+          {
+            F3_T0();
+            mbar_wait(&a_rdy[s], rph[s]);
+            F3_ACC(ph_sa);
+          }
           rph[s] ^= 1;
           const int64_t tile = 4 * pi + 2 * s + rank;
           // layer l's input for the dW GEMM (l = 0: the GRFF features, unless the dW GEMM recomputes them)
-          if (l > 0 || p.stash_feat) {
+          if (!p.zall && (l > 0 || p.stash_feat)) {
             bulk_s2g(p.hstash + ((size_t)l * p.n_tiles + tile) * A_BYTES, sA0 + s * A_BYTES, A_BYTES);
             bulk_commit();
+            F3_T0();
             bulk_wait_read_all();
+            F3_ACC(ph_sr);
           }
           mbar_arrive(&acc_full[s]);
         }
       }
     }
     bulk_wait_all();
+#ifdef DINR_PHASES
+    if (p.dbg) {
+      p.dbg[(size_t)blockIdx.x * 32 + 12] = ph_sa;
+      p.dbg[(size_t)blockIdx.x * 32 + 13] = ph_sr;
+    }
+#endif
   } else if (tid < 512) {
     // ============================================================ epilogue streams
     const int s = tid >> 8, wt = tid & 255;
@@ -180,6 +229,7 @@ __global__ void __launch_bounds__(Fwd3Layout::NT, 1) k_tc_fwd3(TcParams p) {
     const uint32_t a_full_leader = mapa_shared(smem_u32(&a_full[s]), 0);
     const uint64_t pol_z = policy_evict_first();
     uint32_t accph = 0;
+    [[maybe_unused]] unsigned long long ph_e[4] = {0, 0, 0, 0};  // features, acc wait, layer epilogue, head sum
     auto hand_off = [&]() {  // A_s written (generic proxy) -> the pair MMA and this CTA's stash store
       fence_proxy_async_smem();
       asm volatile("bar.sync %0, 256;" ::"r"(1 + s) : "memory");
@@ -197,6 +247,7 @@ __global__ void __launch_bounds__(Fwd3Layout::NT, 1) k_tc_fwd3(TcParams p) {
       const bool valid = g < p.nsamp;
       // ---------------------------------------------------------------- a5/a6 features (as K2)
       {
+        F3_T0();
         float rb0 = 0.f, rb1 = 0.f, rb2 = 0.f, rb3 = 0.f;
         if (valid) {
           int64_t ray = ray_of(g, p.n_s);
@@ -231,15 +282,21 @@ __global__ void __launch_bounds__(Fwd3Layout::NT, 1) k_tc_fwd3(TcParams p) {
                          ps[4 * hh + 3]);
           }
         }
+        F3_ACC(ph_e[0]);
       }
       hand_off();
       // ---------------------------------------------------------------- a7/a8 layers
       float mu_acc = 0.f;
       for (int l = 0; l < L; ++l) {
         const bool last = (l == L - 1);
-        mbar_wait_cluster(&acc_full[s], accph);
+        {
+          F3_T0();
+          mbar_wait(&acc_full[s], accph);  // CTA scope: TMEM + own smem only
+          F3_ACC(ph_e[1]);
+        }
         accph ^= 1;
         tc_fence_after();
+        F3_T0();
 #pragma unroll 1
         for (int cb = cg * 4; cb < cg * 4 + 4; ++cb) {  // this thread's 32-column chunks
 #pragma unroll
@@ -248,6 +305,34 @@ __global__ void __launch_bounds__(Fwd3Layout::NT, 1) k_tc_fwd3(TcParams p) {
             tmem_ld16(tmem_row + cb * 32 + q16 * 16, v);
             tmem_wait_ld();
             const int col0 = cb * 32 + q16 * 16;
+            if (p.zall) {
+              // y = z / 2, h = swish(z) = y (1 + tanh y); backward state: fp16 y of every layer
+              float y[16], hv[16];
+#pragma unroll
+              for (int i = 0; i < 16; ++i) {
+                y[i] = fmaf(__uint_as_float(v[i]), 0.5f, sBias[l * H + col0 + i]);
+                hv[i] = fmaf(y[i], tanh_approx(y[i]), y[i]);
+              }
+              uint32_t y8[8];
+#pragma unroll
+              for (int e = 0; e < 8; ++e) {
+                __half2 hh = __floats2half2_rn(y[2 * e], y[2 * e + 1]);
+                y8[e] = *reinterpret_cast<uint32_t *>(&hh);
+              }
+              st_global_v8_hint(p.zstash + ((((size_t)l * p.n_tiles + tile) * (H / 16) + (col0 >> 4)) * 128 + row) * 32, y8,
+                                pol_z);
+              if (!last) {
+                uint32_t w8[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) w8[e] = pack_bf16x2(hv[2 * e], hv[2 * e + 1]);
+                st_shared_v4(a_base + sw128_offset(row, col0, 128), w8[0], w8[1], w8[2], w8[3]);
+                st_shared_v4(a_base + sw128_offset(row, col0 + 8, 128), w8[4], w8[5], w8[6], w8[7]);
+              } else {
+#pragma unroll
+                for (int i = 0; i < 16; ++i) mu_acc += sWo[col0 + i] * hv[i];
+              }
+              continue;
+            }
             float z[16], sg[16];
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
@@ -283,6 +368,7 @@ __global__ void __launch_bounds__(Fwd3Layout::NT, 1) k_tc_fwd3(TcParams p) {
         }
         tc_fence_before();
         if (!last) hand_off();
+        F3_ACC(ph_e[2]);
       }
       // a9 ray-chunk sum of M = mu0 (w_o . h_L + b_o) over each warp's 32 samples
       sMu[(s * 2 + cg) * 128 + row] = mu_acc;
@@ -293,6 +379,10 @@ __global__ void __launch_bounds__(Fwd3Layout::NT, 1) k_tc_fwd3(TcParams p) {
         for (int o = 16; o > 0; o >>= 1) mu += __shfl_xor_sync(0xffffffffu, mu, o);
         if (lane == 0 && valid) p.pchunk[g >> 5] = mu;
       }
+#ifdef DINR_PHASES
+      if (wt == 0 && p.dbg)
+        for (int k = 0; k < 4; ++k) p.dbg[(size_t)blockIdx.x * 32 + s * 4 + k] = ph_e[k];
+#endif
       // the last layer's A_s was not rewritten: the stash thread's arrival for it is still owed
       // (it stores inputs of layers 0 .. L-1 only), so nothing to hand off here
     }

@@ -42,6 +42,11 @@ struct TcParams {
   int grid_mode;
   VoxGrid vg;
   float *vout;
+  unsigned long long *dbg;  // DINR_PHASES builds: per-CTA cycle counters (k_tc_fwd3)
+  // H = 256 split path with k_tc_fwd3: the forward stashes only y_l = z_l / 2 (fp16, every layer;
+  // no h stash, no swish' stash); K3 recomputes swish'(z) and the dW GEMM recomputes h = swish(z)
+  int zall;
+  float *db3;  // zall: per-CTA bias-gradient partials [L][2 m-blocks][gridDim.x][128] (K3's ones-MMA)
 };
 
 template <int H>
@@ -50,7 +55,7 @@ struct TcLayout {
   static constexpr uint32_t W_LAYER = H * H * 2u;
   static size_t smem_bytes(int L, bool resident) {
     size_t w = resident ? (size_t)L * W_LAYER : W_LAYER;
-    return 1024 + A_BYTES + w + (size_t)L * H * 4 + H * 4 + 16 + (H / 2) * 16 + 64 + 2 * 128 * 4;
+    return 1024 + A_BYTES + w + 2048 + (size_t)L * H * 4 + H * 4 + 16 + (H / 2) * 16 + 64 + 2 * 128 * 4;
   }
 };
 
@@ -74,9 +79,12 @@ constexpr int kTcThreads = 256;
 // MODE 1: training forward: as 0, plus bulk stores of every layer input h_l and fp16 z_l stores
 // MODE 2: training backward from the stashes: top-layer delta and head gradients from z_{L-1},
 //         then the dX chain (K3); no forward recompute
+// MODE 3: MODE 2 on the y-only stash of k_tc_fwd3 (H = 256, DINR_ZALL): swish' recomputed from
+//         y = z / 2, and db accumulated by a ones-MMA (the dW GEMM k_tc_dwz has no TMEM for it)
 template <int H, int MODE>
 __global__ void __launch_bounds__(kTcThreads, 1) k_tc_mlp(TcParams p) {
-  constexpr bool TRAIN = MODE == 2;
+  constexpr bool TRAIN = MODE == 2 || MODE == 3;
+  constexpr bool ZALL = MODE == 3;  // MODE 3: MODE 2 on the y-only stash (k_tc_fwd3 zall), H = 256
   constexpr int C = H / 2;
   constexpr uint32_t A_BYTES = TcLayout<H>::A_BYTES;
   constexpr uint32_t W_LAYER = TcLayout<H>::W_LAYER;
@@ -86,17 +94,23 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_mlp(TcParams p) {
   const bool resident = p.resident != 0;
   uint8_t *sA = smem;
   uint8_t *sW = smem + A_BYTES;
-  float *sBias = reinterpret_cast<float *>(sW + (resident ? (size_t)L * W_LAYER : (size_t)W_LAYER));
+  uint8_t *sOnes = sW + (resident ? (size_t)L * W_LAYER : (size_t)W_LAYER);  // K3 zall: bf16 ones (db MMA)
+  float *sBias = reinterpret_cast<float *>(sOnes + 2048);
   float *sWo = sBias + L * H;
   float *sB = sWo + H + 4;
   uint64_t *bars = reinterpret_cast<uint64_t *>(sB + C * 4);
   uint64_t *mma_bar = bars, *w_bar = bars + 2;  // mma_bar[cg]: N-half cg of the current MMA retired
   uint64_t *sa_ok = bars + 3;                    // MODE 1: sA may be rewritten (see the epilogue)
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 4);
+  uint64_t *db_bar = bars + 5;  // (the per-half head partials sMu start after it)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  // K3 on the zall path also accumulates db_l = sum_samples delta_l with a ones-MMA per m-block
+  // into TMEM columns [H, H + 2L 16) for the CTA's life (the dW GEMM then has no room for it)
+  constexpr bool dbm = ZALL && H == 256;
+  const uint32_t tcols = dbm ? 512u : (uint32_t)H;
   if (warp == 0) {
-    tmem_alloc(tmem_slot, H);
+    tmem_alloc(tmem_slot, tcols);
     tmem_relinquish();
   }
   if (tid == 0) {
@@ -104,7 +118,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_mlp(TcParams p) {
     mbar_init(&mma_bar[1], 1);
     mbar_init(w_bar, 1);
     mbar_init(sa_ok, 1);
+    mbar_init(db_bar, 1);
     fence_mbar_init();
+  }
+  if (dbm) {
+    for (int i = tid; i < 2048 / 4; i += kTcThreads) reinterpret_cast<uint32_t *>(sOnes)[i] = 0x3F803F80u;
+    fence_proxy_async_smem();
   }
   const int64_t per = (int64_t)H * H + H;
   for (int i = tid; i < L * H; i += kTcThreads) sBias[i] = p.params[(i / H) * per + (int64_t)H * H + (i % H)];
@@ -118,7 +137,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_mlp(TcParams p) {
   const uint32_t tmem_row = tmem + ((uint32_t)((warp & 3) * 32) << 16);
   const int cg = tid >> 7;                     // column half of this thread
   const int cb_lo = cg * (H / 64);  // first of its H/64 32-column chunks
-  float *sMu = reinterpret_cast<float *>(bars + 5);  // [2][128] per-half head partials (forward)
+  float *sMu = reinterpret_cast<float *>(bars + 6);  // [2][128] per-half head partials (forward)
   // the training plan may round the tile count up (paired tiles): padding tiles hold invalid samples
   const int n_tiles = (int)(p.n_tiles > (p.nsamp + 127) / 128 ? p.n_tiles : (p.nsamp + 127) / 128);
 
@@ -143,7 +162,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_mlp(TcParams p) {
     }
     return resident ? w_base + (uint32_t)layer * W_LAYER : w_base;
   };
-  if (tid == 0 && (int)blockIdx.x < n_tiles && (MODE != 2 || L >= 2)) w_issue(MODE == 2 ? L - 1 : 0);
+  if (tid == 0 && (int)blockIdx.x < n_tiles && (!TRAIN || L >= 2)) w_issue(TRAIN ? L - 1 : 0);
 
   uint32_t mma_phase = 0, sa_phase = 0;
   constexpr int NCB = H / 64;  // 32-column chunks of this thread's column half
@@ -157,17 +176,30 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_mlp(TcParams p) {
   const uint32_t idesc_f = idesc_bf16(128, NH, 0, 0);
   const uint32_t idesc_b = idesc_bf16(128, NH, 0, 1);
 
+  bool db_first = true;  // the CTA's first tile: the db accumulators start fresh
+  uint32_t db_phase = 0;
+  const uint32_t ones_a = smem_u32(sOnes);
+  const uint32_t idesc_db = idesc_bf16(128, 16, 1, 0);  // A = delta^T (MN-major), B = ones (K-major)
+  auto issue_db = [&](int l) {  // thread 0: db_l += sum over the tile's samples of delta_l, per m-block
+    tc_fence_after();
+#pragma unroll
+    for (int mb = 0; mb < 2; ++mb)
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk)
+        umma_bf16(tmem + H + (uint32_t)(l * 2 + mb) * 16, sdesc_sw128(a_base + mb * 32768 + kk * 2048, 16384, 1024),
+                  sdesc_sw128(ones_a + (kk & 3) * 32, 16, 1024), idesc_db, (!db_first || kk > 0) ? 1u : 0u);
+  };
   for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
     const bool more_tiles = tile + (int)gridDim.x < n_tiles;
     const int row = tid & 127;
     const int64_t g = (int64_t)tile * 128 + row;
     const bool valid = g < p.nsamp;
     bool inside = false;
-    if (MODE == 2) {  // the previous tile's last bulk store must be done reading sA
+    if (TRAIN) {  // the previous tile's last bulk store must be done reading sA
       if (tid == 0) bulk_wait_read_all();
       __syncthreads();
     }
-    if (MODE != 2) {
+    if (!TRAIN) {
       // ---------------------------------------------------------------- a5/a6 features
       {
         float rb0 = 0.f, rb1 = 0.f, rb2 = 0.f, rb3 = 0.f;
@@ -337,6 +369,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_mlp(TcParams p) {
       // top layer from the stashed z_{L-1}: h_L = swish(z) for the head gradients (transpose-
       // reduce u h_L over the warp's 32 rows), delta_L = u w_o swish'(z)
       const float u_row = valid ? p.u[ray_of(g, p.n_s)] : 0.f;
+      constexpr float zscale = ZALL ? 2.f : 1.f;
       constexpr uint32_t kZTile = 128u * H * 2u;  // one tile of fp16 z
       if (tid == 0 && L >= 2)  // z_{L-2} is read after the first dX: bring it to L2 now
         bulk_prefetch_l2(p.zstash + ((size_t)(L - 2) * p.n_tiles + tile) * kZTile, kZTile);
@@ -359,8 +392,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_mlp(TcParams p) {
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               const float2 zf = __half22float2(*reinterpret_cast<const __half2 *>(&zz[e]));
-              z[8 * q + 2 * e] = zf.x;
-              z[8 * q + 2 * e + 1] = zf.y;
+              z[8 * q + 2 * e] = zscale * zf.x;  // zall: the stash holds y = z / 2 (exact scaling)
+              z[8 * q + 2 * e + 1] = zscale * zf.y;
             }
           }
           float x[32];
@@ -396,6 +429,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_mlp(TcParams p) {
         if (tid == 0) {
           bulk_s2g(p.dstash + ((size_t)(L - 1) * p.n_tiles + tile) * A_BYTES, sA, A_BYTES);
           bulk_commit();
+          if (dbm) issue_db(L - 1);
         }
       }
       if (cg == 0) {
@@ -462,7 +496,17 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_mlp(TcParams p) {
 #pragma unroll
             for (int e = 0; e < 4; ++e) {  // delta = e swish'(z), swish' stashed as bf16 by the forward
               int i0 = 8 * q + 2 * e;
-              w4[e] = pack_bf16x2(__uint_as_float(v[i0]) * bf16lo(zz[e]), __uint_as_float(v[i0 + 1]) * bf16hi(zz[e]));
+              float s0, s1;
+              if (ZALL) {  // swish'(z) from the stashed y = z / 2: s = (1 + tanh y) / 2, s (1 + 2 y (1 - s))
+                const float2 yf = __half22float2(*reinterpret_cast<const __half2 *>(&zz[e]));
+                const float g0 = fmaf(0.5f, tanh_approx(yf.x), 0.5f), g1 = fmaf(0.5f, tanh_approx(yf.y), 0.5f);
+                s0 = fmaf(g0, 2.f * yf.x * (1.f - g0), g0);
+                s1 = fmaf(g1, 2.f * yf.y * (1.f - g1), g1);
+              } else {
+                s0 = bf16lo(zz[e]);
+                s1 = bf16hi(zz[e]);
+              }
+              w4[e] = pack_bf16x2(__uint_as_float(v[i0]) * s0, __uint_as_float(v[i0 + 1]) * s1);
             }
             st_shared_v4(a_base + sw128_offset(row, cb * 32 + 8 * q, 128), w4[0], w4[1], w4[2], w4[3]);
           }
@@ -473,11 +517,33 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_mlp(TcParams p) {
         if (tid == 0) {
           bulk_s2g(p.dstash + ((size_t)(l - 1) * p.n_tiles + tile) * A_BYTES, sA, A_BYTES);
           bulk_commit();
+          if (dbm) issue_db(l - 1);
         }
       }
+      if (dbm && tid == 0) {  // delta_0's db MMAs must retire before the next tile rewrites sA
+        umma_commit(db_bar);
+        mbar_wait(db_bar, db_phase);
+        db_phase ^= 1;
+      }
+      db_first = false;
     }
   }
   if (TRAIN) {
+    // thread 0 waited for the last db MMAs (db_bar): order the other warps' TMEM reads after it
+    tc_fence_before();
+    __syncthreads();
+    if (dbm && warp < 4) {  // db partials: TMEM lane o = output feature o of m-block mb
+      tc_fence_after();
+      for (int l = 0; l < L; ++l)
+#pragma unroll
+        for (int mb = 0; mb < 2; ++mb) {
+          uint32_t v[16];
+          tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + H + (uint32_t)(l * 2 + mb) * 16, v);
+          tmem_wait_ld();
+          p.db3[(((size_t)l * 2 + mb) * gridDim.x + blockIdx.x) * 128 + warp * 32 + lane] =
+              db_first ? 0.f : __uint_as_float(v[0]);
+        }
+    }
     // per-CTA head partials: [H] = dL/dw_o, [H] slot = dL/db_o; combine the 4 warps via smem
     __syncthreads();
     float *red = reinterpret_cast<float *>(sA);  // A tile is free now (all bulk reads waited below)
@@ -499,7 +565,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_mlp(TcParams p) {
   __syncthreads();
   if (warp == 0) {
     tc_fence_after();
-    tmem_dealloc(tmem, H);
+    tmem_dealloc(tmem, tcols);
   }
 }
 
