@@ -59,7 +59,7 @@ def profiled_traffic(workload, kernel_class, path_kind):
     (profiles/traffic.json, written by tools/ncu_summary.py traffic), or None if that capture is
     not for this workload / kernel."""
     names = {"backward": {0: "k_tc_mlp", 1: "k_fused<", 2: "k_fused2<"}.get(path_kind, ""), "dw": "k_tc_dw",
-             "forward": "k_tc_mlp", "rays": "k_ray_setup", "loss": "k_loss"}
+             "forward": "k_tc_fwd", "rays": "k_ray_setup", "loss": "k_loss"}
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
             tr = json.load(fh)
@@ -241,6 +241,9 @@ def main():
     ap.add_argument("--combine", default="beer", choices=["beer", "linear"])
     ap.add_argument("--strong", action="store_true",
                     help="strong scaling: the workload's batch is the global batch, split over the ranks")
+    ap.add_argument("--full-step", action="store_true",
+                    help="time the N1 epoch loop's iteration (sampler + gather + step + all-reduce + Adam at the "
+                         "epoch's lr) through dinr_train_iterations on a resident view-sharded y")
     ap.add_argument("--launch-dry-run", action="store_true",
                     help="spawn the ranks, have each print its rank and world size, and exit (no GPU work)")
     args = ap.parse_args()
@@ -317,7 +320,26 @@ def main():
     adam_v = torch.zeros(P, device=dev)
     adam_t = [0]
 
+    full = None
+    if args.full_step:
+        # N1 epoch loop (R27): every step samples this rank's pixels from its view
+        # shard without replacement (per-epoch permutation), gathers y from the resident shard,
+        # then local loss + gradient, all-reduce, Adam at lr0 0.95^epoch -- one dinr_train_iterations
+        # call.  y shard: seeded uniform values (the work does not depend on them), view by view.
+        M_, N_ = len(th), g["n_rows"] * g["n_cols"]
+        nv = len(range(rank, M_, world))
+        y_shard = torch.empty(nv * N_, device=dev)
+        y_shard.uniform_(0.0, 1.0, generator=torch.Generator(device=dev).manual_seed(77 + rank))
+        desc = D.train_desc(seed=2024, batch=n, rank=rank, world=world, sharding="views")
+        full = dict(y=y_shard, desc=desc, loss=torch.zeros(1, device=dev), g=[0],
+                    ipe=D.iterations_per_epoch(ctx, desc))
+
     def step(q):
+        if full is not None:
+            D.train_iterations(ctx, full["desc"], full["g"][0], 1, full["y"], params, adam_m, adam_v, grad, full["loss"],
+                               stream=stream)
+            full["g"][0] += 1
+            return
         # one training step: local loss + gradient, gradient average across the
         # ranks, then Adam (lr 1e-3) fused with the re-pack of the bf16 weight images
         D.project_and_grad(ctx, idx_pool[q % pool], y_pool[q % pool], grad, stream=stream)
@@ -452,7 +474,10 @@ def main():
             "config": {"workload": name, "pixels_per_gpu": n, "sub_rays": S, "samples_per_ray": ns,
                        "mlp": f"{L}x{H}", "params": P, "samples_per_step": samples_per_step,
                        "combine": args.combine, "l2": "flushed (256 MiB write) before every timed step",
-                       "parallelism": f"dp{world}"},
+                       "parallelism": f"dp{world}",
+                       "step": ("N1 epoch-loop iteration: sample + gather + project_and_grad + allreduce + Adam"
+                                f" (dinr_train_iterations, {full['ipe']} iterations/epoch)" if full is not None else
+                                "project_and_grad + allreduce + Adam on resident batches")},
             "roofline": roof,
             "step_roofline": {"flop_per_sample": fps, "achieved_tflops": step_tflops,
                               "frac_burst": step_tflops / tf_burst,

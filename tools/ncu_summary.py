@@ -60,26 +60,29 @@ def launches(path):
         print(f"{k[:60]:60s} {cnt[k]:8d} {tot[k]:12.1f} {tot[k] / cnt[k]:12.1f} {100 * tot[k] / allt:6.1f}%")
 
 
-def traffic(path, workload):
-    """dram__bytes_read.sum + dram__bytes_write.sum per profiled kernel (first launch of each)."""
+def traffic(*args):
+    """dram__bytes_read.sum + dram__bytes_write.sum per profiled kernel (first launch of each):
+    traffic <report.ncu-rep> [<report2.ncu-rep> ...] <workload>"""
     import json
     import os
 
-    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
-    rows = list(csv.reader(out.splitlines()))
-    hdr, units = rows[0], rows[1]
-    col = {h: i for i, h in enumerate(hdr)}
+    *paths, workload = args
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
     kern = {}
-    for r in rows[2:]:
-        name = r[col["Kernel Name"]]
-        if name in kern:
-            continue
-        tot = 0.0
-        for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
-            tot += float(r[col[m]].replace(",", "")) * scale.get(units[col[m]], 1)
-        kern[name] = tot
-    res = {"workload": workload, "source": os.path.basename(path), "kernels": kern}
+    for path in paths:
+        out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+        rows = list(csv.reader(out.splitlines()))
+        hdr, units = rows[0], rows[1]
+        col = {h: i for i, h in enumerate(hdr)}
+        for r in rows[2:]:
+            name = r[col["Kernel Name"]]
+            if name in kern:
+                continue
+            tot = 0.0
+            for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                tot += float(r[col[m]].replace(",", "")) * scale.get(units[col[m]], 1)
+            kern[name] = tot
+    res = {"workload": workload, "source": [os.path.basename(p) for p in paths], "kernels": kern}
     dst = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "traffic.json")
     with open(dst, "w") as fh:
         json.dump(res, fh, indent=1)
