@@ -85,14 +85,27 @@ struct Launch {
 
 bool is_fin(double x) { return std::isfinite(x); }
 
-// Carve a scratch arena into 256-B aligned pieces.
+// Carve a scratch arena into 256-B aligned pieces.  With DINR_GUARDS set (a debugging mode: the
+// pool has no compute-sanitizer), every piece is preceded by a 4 KB guard band that ensure_plan fills
+// with 0xA5 and dinr_get_device_status checks: any write past the end of a scratch buffer lands in a
+// band and is reported as DINR_EDEVICE.
+constexpr size_t kGuardBytes = 4096;
+bool guards_on() {
+  static const bool on = std::getenv("DINR_GUARDS") != nullptr;
+  return on;
+}
 struct Arena {
   uint8_t *base;
   size_t off = 0;
+  std::vector<size_t> *bands = nullptr;  // guard band offsets (DINR_GUARDS)
   explicit Arena(void *b) : base((uint8_t *)b) {}
   template <class T>
   T *take(size_t count) {
     off = (off + 255) & ~size_t(255);
+    if (guards_on()) {
+      if (bands) bands->push_back(off);
+      off += kGuardBytes;
+    }
     T *p = base ? reinterpret_cast<T *>(base + off) : nullptr;
     off += count * sizeof(T);
     return p;
@@ -168,8 +181,10 @@ int tc_occupancy(const dinr_ctx *c) {
 
 bool tc_resident(int H, int L) { return (size_t)L * H * H * 2 + (size_t)H * 256 <= 180 * 1024; }
 
-size_t plan_layout(dinr_ctx *c, int64_t n, bool train, bool host_io, Plan &pl, void *base) {
+size_t plan_layout(dinr_ctx *c, int64_t n, bool train, bool host_io, Plan &pl, void *base,
+                   std::vector<size_t> *bands = nullptr) {
   Arena ar(base);
+  ar.bands = bands;
   pl.n = n;
   pl.n_rays = n * c->S;
   pl.nsamp = pl.n_rays * c->geom.samples_per_ray;
@@ -303,8 +318,32 @@ dinr_status ensure_plan(dinr_ctx *c, int64_t n, bool train, bool host_io, Plan &
     }
     c->scratch_cap = cap;
   }
+  if (guards_on()) {
+    std::vector<size_t> bands;
+    plan_layout(c, n, train, host_io, pl, c->scratch, &bands);
+    bands.push_back((need - 1024 + 255) & ~size_t(255));  // tail band: after the last buffer (inside the slack)
+    c->guard_bands = bands;
+    for (size_t b : bands)
+      if (b + kGuardBytes <= c->scratch_cap) CUDA_TRY(c, cudaMemset((uint8_t *)c->scratch + b, 0xA5, kGuardBytes));
+    return DINR_OK;
+  }
   plan_layout(c, n, train, host_io, pl, c->scratch);
   return DINR_OK;
+}
+
+// DINR_GUARDS: every guard band still holds 0xA5 (checked by dinr_get_device_status)
+bool guards_intact(dinr_ctx *c, size_t *bad) {
+  std::vector<uint8_t> h(kGuardBytes);
+  for (size_t b : c->guard_bands) {
+    if (b + kGuardBytes > c->scratch_cap) continue;
+    if (cudaMemcpy(h.data(), (uint8_t *)c->scratch + b, kGuardBytes, cudaMemcpyDeviceToHost) != cudaSuccess) return false;
+    for (size_t i = 0; i < kGuardBytes; ++i)
+      if (h[i] != 0xA5) {
+        *bad = b + i;
+        return false;
+      }
+  }
+  return true;
 }
 
 GeomParams geom_params(const dinr_ctx *c) {
@@ -1316,10 +1355,13 @@ dinr_status dinr_get_device_status(dinr_ctx *c) {
   if (!c) return DINR_EINVAL;
   CUDA_TRY(c, cudaSetDevice(c->device));
   CUDA_TRY(c, cudaDeviceSynchronize());
-  int flags = 0;
-  CUDA_TRY(c, cudaMemcpy(&flags, c->d_flags, sizeof(int), cudaMemcpyDeviceToHost));
-  CUDA_TRY(c, cudaMemset(c->d_flags, 0, sizeof(int)));
-  if (flags & 1) return fail(c, DINR_ERANGE, "a pixel index was out of range (>= M*N); it contributed 0");
+  int flags[1] = {0};
+  CUDA_TRY(c, cudaMemcpy(flags, c->d_flags, sizeof(flags), cudaMemcpyDeviceToHost));
+  CUDA_TRY(c, cudaMemset(c->d_flags, 0, sizeof(flags)));
+  size_t bad = 0;
+  if (guards_on() && !guards_intact(c, &bad))
+    return fail(c, DINR_EDEVICE, "DINR_GUARDS: scratch guard band overwritten at byte " + std::to_string(bad));
+  if (flags[0] & 1) return fail(c, DINR_ERANGE, "a pixel index was out of range (>= M*N); it contributed 0");
   return DINR_OK;
 }
 

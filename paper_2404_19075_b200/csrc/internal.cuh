@@ -78,6 +78,7 @@ struct dinr_ctx {
   // scratch (grown on demand)
   void *scratch = nullptr;
   size_t scratch_cap = 0;
+  std::vector<size_t> guard_bands;  // DINR_GUARDS: offsets of the 4 KB bands around the plan's buffers
   int *d_flags = nullptr;  // [0] = out-of-range index seen
   float *d_ones = nullptr;
   void *d_prims = nullptr;  // N2 phantom primitives (64 slots)

@@ -47,7 +47,8 @@ def step(name, n, over=None, fover=None, precision="bf16", extra=False):
         vox = torch.zeros(gr["nx"] * gr["ny"] * 2, device=dev)
         D.voxelize(ctx, gr, 0.0, 0, 2, vox)
     torch.cuda.synchronize()
-    assert D.get_device_status(ctx) == 0
+    st = D.get_device_status(ctx)
+    assert st == 0, (st, D.load().dinr_last_error(ctx))
     D.destroy(ctx)
     print("ok", name, n, over, fover, precision, flush=True)
 
