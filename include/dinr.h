@@ -78,7 +78,8 @@ typedef enum { DINR_MIDPOINT = 0, DINR_JITTER = 1 } dinr_sampling;
  *   the detector z extent [-C_z, -C_z + n_rows dz], scaled for cone beam by (sod + r)/(sod + odd)
  *   (the far side of the FOV cylinder); NaN t_lo / t_hi: the first / last view time.
  * Invariants: sod > 0, odd >= 0, pixel pitches > 0, fov_radius > 0,
- *   fov_radius < sod, sub_x, sub_z >= 1, samples_per_ray >= 32 and a multiple of 32,
+ *   fov_radius < sod, sub_x, sub_z >= 1, samples_per_ray >= 1 (a multiple of 32 on the BF16 path,
+ *   checked by whichever of set_geometry / set_field_weights comes second),
  *   n_rows, n_cols >= 1, z_hi >= z_lo, t_hi >= t_lo. */
 typedef struct {
   int32_t beam;            /* dinr_beam */

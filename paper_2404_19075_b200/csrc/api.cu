@@ -133,6 +133,7 @@ struct Plan {
   uint2 *rid;   // global ray ids (N3 keys)
   Jitter jit;   // N3 sample placement handed to the MLP kernels
   float *pchunk, *u, *fhat, *loss_part, *head_part, *dw_part, *db_part, *colsum;
+  float *smu;  // fp32 verify with N_s % 32 != 0: per-sample mu before the per-ray sums
   float *db3;  // zall: K3's per-CTA bias-gradient partials [L][2][grid_tc][128]
   float *wq;  // per-ray quadrature weight (K1 -> K4)
   uint8_t *hstash, *dstash, *zstash;
@@ -188,7 +189,9 @@ size_t plan_layout(dinr_ctx *c, int64_t n, bool train, bool host_io, Plan &pl, v
   pl.n = n;
   pl.n_rays = n * c->S;
   pl.nsamp = pl.n_rays * c->geom.samples_per_ray;
-  pl.nc = c->geom.samples_per_ray / kChunk;
+  // ray-sum partials per ray: 32-sample chunks, or (fp32 verify with N_s not a multiple of 32) one per ray
+  const bool whole_warps = c->geom.samples_per_ray % kChunk == 0;
+  pl.nc = whole_warps ? c->geom.samples_per_ray / kChunk : 1;
   pl.n_tiles = (pl.nsamp + 127) / 128;
   pl.grid_tc = (int)std::max<int64_t>(1, std::min<int64_t>(pl.n_tiles, (int64_t)c->sm_count * tc_occupancy(c)));
   pl.nmb = c->H == 256 ? 2 : 1;
@@ -205,7 +208,8 @@ size_t plan_layout(dinr_ctx *c, int64_t n, bool train, bool host_io, Plan &pl, v
   pl.jit.seed_lo = (uint32_t)c->seed;
   pl.jit.seed_hi = (uint32_t)(c->seed >> 32);
   pl.jit.step = c->step;
-  pl.pchunk = ar.take<float>(pl.nsamp / kChunk + 1);
+  pl.pchunk = ar.take<float>(whole_warps ? pl.nsamp / kChunk + 1 : pl.n_rays + 1);
+  pl.smu = whole_warps ? nullptr : ar.take<float>(pl.nsamp + 1);
   pl.u = ar.take<float>(pl.n_rays + 1);
   pl.wq = ar.take<float>(pl.n_rays + 1);
   pl.fhat = ar.take<float>(n + 1);
@@ -731,7 +735,12 @@ dinr_status simt_forward(dinr_ctx *c, const Plan &pl, cudaStream_t st) {
   {
     Launch L_(c, T_FWD, st);
     s_head<<<(unsigned)((ns + 255) / 256), 256, 0, st>>>(pl.sh + (size_t)L * ns * H, ns, H,
-                                                       c->d_params + L * per, (float)c->field.mu0, pl.pchunk);
+                                                       c->d_params + L * per, (float)c->field.mu0,
+                                                       pl.smu ? nullptr : pl.pchunk, pl.smu);
+  }
+  if (pl.smu) {  // N_s not a multiple of 32: per-ray sums in fixed order
+    Launch L_(c, T_FWD, st);
+    s_raysum<<<(unsigned)((pl.n_rays + 255) / 256), 256, 0, st>>>(pl.smu, pl.n_rays, c->geom.samples_per_ray, pl.pchunk);
   }
   CUDA_TRY(c, cudaGetLastError());
   return DINR_OK;
@@ -981,8 +990,12 @@ dinr_status dinr_set_geometry(dinr_ctx *c, const dinr_geometry *g_in, const doub
   if (g->n_rows < 1 || g->n_cols < 1) return fail(c, DINR_EINVAL, "n_rows, n_cols must be >= 1");
   if (g->sub_x < 1 || g->sub_z < 1 || g->sub_x * g->sub_z > kMaxS)
     return fail(c, DINR_EINVAL, "sub_x, sub_z must be >= 1 with sub_x*sub_z <= 16");
-  if (g->samples_per_ray < 32 || g->samples_per_ray % 32)
-    return fail(c, DINR_EINVAL, "samples_per_ray must be a positive multiple of 32");
+  // N_s: any N_s >= 1 on the fp32 verify path; a multiple of 32 on the bf16 tensor-core path (the
+  // performance contract: a ray is whole warps), checked here when the weights are already set and
+  // by dinr_set_field_weights otherwise
+  if (g->samples_per_ray < 1) return fail(c, DINR_EINVAL, "samples_per_ray must be >= 1");
+  if (c->have_field && c->field.precision == DINR_BF16 && g->samples_per_ray % 32)
+    return fail(c, DINR_EINVAL, "the BF16 path needs samples_per_ray a multiple of 32 (FP32_VERIFY accepts any)");
   const double v[] = {g->sod, g->odd, g->pixel_dx, g->pixel_dz, g->offset_cx, g->offset_cz, g->fov_radius,
                       g->rot_center_x, g->z_lo, g->z_hi, g->t_lo, g->t_hi};
   for (double x : v)
@@ -1030,6 +1043,8 @@ dinr_status dinr_set_field_weights(dinr_ctx *c, const dinr_field_desc *f, const 
   if (f->precision == DINR_BF16) {
     if (f->width != 64 && f->width != 128 && f->width != 256)
       return fail(c, DINR_EINVAL, "BF16 path supports width 64, 128 or 256");
+    if (c->geom.samples_per_ray % 32)
+      return fail(c, DINR_EINVAL, "the BF16 path needs samples_per_ray a multiple of 32 (FP32_VERIFY accepts any)");
   } else if (f->precision == DINR_FP32_VERIFY) {
     if (f->width > kMaxH || f->width % 2) return fail(c, DINR_EINVAL, "FP32_VERIFY supports width <= 256");
   } else {

@@ -114,8 +114,10 @@ __global__ void __launch_bounds__(256) s_gemm(SgemmArgs a) {
 }
 
 // Ray chunk sums of M = mu0 (w_o . h_L + b_o): one warp per 32 samples.
+// mu per sample: 32-sample chunk sums into pchunk, or (smu != null: N_s not a multiple of 32) the
+// per-sample values into smu for s_raysum
 __global__ void s_head(const float *__restrict__ hL, int64_t nsamp, int H, const float *__restrict__ wo,
-                       float mu0, float *__restrict__ pchunk) {
+                       float mu0, float *__restrict__ pchunk, float *__restrict__ smu) {
   const float bo = wo[H];
   int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   float mu = 0.f;
@@ -125,8 +127,21 @@ __global__ void s_head(const float *__restrict__ hL, int64_t nsamp, int H, const
     for (int k = 0; k < H; ++k) acc += wo[k] * h[k];
     mu = mu0 * (acc + bo);
   }
+  if (smu) {
+    if (g < nsamp) smu[g] = mu;
+    return;
+  }
   for (int o = 16; o > 0; o >>= 1) mu += __shfl_xor_sync(0xffffffffu, mu, o);
   if ((threadIdx.x & 31) == 0 && g < nsamp) pchunk[g >> 5] = mu;
+}
+
+// per-ray sums of mu (fixed order), one ray per thread
+__global__ void s_raysum(const float *__restrict__ smu, int64_t n_rays, int n_s, float *__restrict__ psum) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n_rays) return;
+  float acc = 0.f;
+  for (int j = 0; j < n_s; ++j) acc += smu[r * n_s + j];
+  psum[r] = acc;
 }
 
 // N4 voxels: mu = mu0 (w_o . h_L + b_o) per voxel, 0 outside the FOV cylinder (R25).

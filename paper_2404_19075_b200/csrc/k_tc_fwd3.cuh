@@ -87,8 +87,8 @@ __global__ void __launch_bounds__(Fwd3Layout::NT, 1) k_tc_fwd3(TcParams p) {
     fence_mbar_init();
   }
   const int64_t per = (int64_t)H * H + H;
-  // zall: the epilogue works on y = z / 2 = 0.5 acc + 0.5 b (one FFMA), so the bias is stored halved
-  const float bscale = p.zall ? 0.5f : 1.f;
+  // the epilogue works on y = z / 2 = 0.5 acc + 0.5 b (one FFMA), so the bias is stored halved
+  const float bscale = 0.5f;
   for (int i = tid; i < L * H; i += LY::NT) sBias[i] = bscale * p.params[(i / H) * per + (int64_t)H * H + (i % H)];
   for (int i = tid; i <= H; i += LY::NT) sWo[i] = p.params[(int64_t)L * per + i];
   for (int i = tid; i < C * 4; i += LY::NT) sB[i] = p.B[i];
@@ -299,70 +299,57 @@ __global__ void __launch_bounds__(Fwd3Layout::NT, 1) k_tc_fwd3(TcParams p) {
         F3_T0();
 #pragma unroll 1
         for (int cb = cg * 4; cb < cg * 4 + 4; ++cb) {  // this thread's 32-column chunks
+          uint32_t va[16], vb[16];  // both 16-column halves of the chunk in flight at once
+          tmem_ld16(tmem_row + cb * 32, va);
+          tmem_ld16(tmem_row + cb * 32 + 16, vb);
+          tmem_wait_ld();
+          reg_fence(va);
+          reg_fence(vb);
 #pragma unroll
           for (int q16 = 0; q16 < 2; ++q16) {
-            uint32_t v[16];
-            tmem_ld16(tmem_row + cb * 32 + q16 * 16, v);
-            tmem_wait_ld();
+            const uint32_t(&v)[16] = q16 ? vb : va;
             const int col0 = cb * 32 + q16 * 16;
-            if (p.zall) {
-              // y = z / 2, h = swish(z) = y (1 + tanh y); backward state: fp16 y of every layer
-              float y[16], hv[16];
+            // y = z / 2 (halved bias), t = tanh y: h = swish(z) = y (1 + t); sigma = (1 + t) / 2;
+            // swish'(z) = sigma (1 + z (1 - sigma)) = sigma + sigma y (1 - t)
+            float y[16], t[16];
 #pragma unroll
-              for (int i = 0; i < 16; ++i) {
-                y[i] = fmaf(__uint_as_float(v[i]), 0.5f, sBias[l * H + col0 + i]);
-                hv[i] = fmaf(y[i], tanh_approx(y[i]), y[i]);
-              }
-              uint32_t y8[8];
+            for (int i = 0; i < 16; ++i) {
+              y[i] = fmaf(__uint_as_float(v[i]), 0.5f, sBias[l * H + col0 + i]);
+              t[i] = tanh_approx(y[i]);
+            }
+            uint32_t s8[8];  // backward state, [16-column chunk][row][32 B] (the layout K3 reads)
+            if (p.zall) {    // fp16 y of every layer
 #pragma unroll
               for (int e = 0; e < 8; ++e) {
                 __half2 hh = __floats2half2_rn(y[2 * e], y[2 * e + 1]);
-                y8[e] = *reinterpret_cast<uint32_t *>(&hh);
+                s8[e] = *reinterpret_cast<uint32_t *>(&hh);
               }
-              st_global_v8_hint(p.zstash + ((((size_t)l * p.n_tiles + tile) * (H / 16) + (col0 >> 4)) * 128 + row) * 32, y8,
-                                pol_z);
-              if (!last) {
-                uint32_t w8[8];
+            } else if (last) {  // fp16 z_{L-1} (= 2 y exactly)
 #pragma unroll
-                for (int e = 0; e < 8; ++e) w8[e] = pack_bf16x2(hv[2 * e], hv[2 * e + 1]);
-                st_shared_v4(a_base + sw128_offset(row, col0, 128), w8[0], w8[1], w8[2], w8[3]);
-                st_shared_v4(a_base + sw128_offset(row, col0 + 8, 128), w8[4], w8[5], w8[6], w8[7]);
-              } else {
-#pragma unroll
-                for (int i = 0; i < 16; ++i) mu_acc += sWo[col0 + i] * hv[i];
+              for (int e = 0; e < 8; ++e) {
+                __half2 hh = __floats2half2_rn(2.f * y[2 * e], 2.f * y[2 * e + 1]);
+                s8[e] = *reinterpret_cast<uint32_t *>(&hh);
               }
-              continue;
-            }
-            float z[16], sg[16];
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              z[i] = __uint_as_float(v[i]) + sBias[l * H + col0 + i];
-              sg[i] = 0.5f + 0.5f * tanh_approx(0.5f * z[i]);
-            }
-            {  // backward state, [16-column chunk][row][32 B] (the layout K3 reads)
-              uint32_t h8[8];
+            } else {  // bf16 swish'(z)
 #pragma unroll
               for (int e = 0; e < 8; ++e) {
                 const int i0 = 2 * e;
-                if (last) {
-                  __half2 hh = __floats2half2_rn(z[i0], z[i0 + 1]);
-                  h8[e] = *reinterpret_cast<uint32_t *>(&hh);
-                } else {
-                  h8[e] = pack_bf16x2(sg[i0] * (1.f + z[i0] * (1.f - sg[i0])), sg[i0 + 1] * (1.f + z[i0 + 1] * (1.f - sg[i0 + 1])));
-                }
+                const float s0 = fmaf(t[i0], 0.5f, 0.5f), s1 = fmaf(t[i0 + 1], 0.5f, 0.5f);
+                s8[e] = pack_bf16x2(fmaf(s0, fmaf(-y[i0], t[i0], y[i0]), s0), fmaf(s1, fmaf(-y[i0 + 1], t[i0 + 1], y[i0 + 1]), s1));
               }
-              st_global_v8_hint(p.zstash + ((((size_t)l * p.n_tiles + tile) * (H / 16) + (col0 >> 4)) * 128 + row) * 32, h8,
-                                pol_z);
             }
+            st_global_v8_hint(p.zstash + ((((size_t)l * p.n_tiles + tile) * (H / 16) + (col0 >> 4)) * 128 + row) * 32, s8,
+                              pol_z);
             if (!last) {
               uint32_t w8[8];
 #pragma unroll
-              for (int e = 0; e < 8; ++e) w8[e] = pack_bf16x2(z[2 * e] * sg[2 * e], z[2 * e + 1] * sg[2 * e + 1]);
+              for (int e = 0; e < 8; ++e)
+                w8[e] = pack_bf16x2(fmaf(y[2 * e], t[2 * e], y[2 * e]), fmaf(y[2 * e + 1], t[2 * e + 1], y[2 * e + 1]));
               st_shared_v4(a_base + sw128_offset(row, col0, 128), w8[0], w8[1], w8[2], w8[3]);
               st_shared_v4(a_base + sw128_offset(row, col0 + 8, 128), w8[4], w8[5], w8[6], w8[7]);
             } else {
 #pragma unroll
-              for (int i = 0; i < 16; ++i) mu_acc += sWo[col0 + i] * (z[i] * sg[i]);
+              for (int i = 0; i < 16; ++i) mu_acc = fmaf(sWo[col0 + i], fmaf(y[i], t[i], y[i]), mu_acc);
             }
           }
         }

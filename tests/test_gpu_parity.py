@@ -378,3 +378,24 @@ def test_nan_normalization_box_is_derived(ctx, dev, name):
     D.project(ctx, idx, b)
     torch.cuda.synchronize()
     assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("n_s", [7, 48])
+def test_fp32_verify_any_samples_per_ray(ctx, dev, O, n_s):
+    """the fp32 verify path accepts any N_s >= 1 (per-ray sums instead of 32-sample
+    chunks); the bf16 path keeps N_s a multiple of 32 and rejects the combination."""
+    g, th, t, f, B, prm = setup_case(ctx, dev, "fan512", dict(n_s=n_s), dict(C=32, L=2), "fp32_verify", "beer")
+    idx = synth.pixel_batch("fan512", 9, seed=3)
+    y = synth.synthetic_y(9, 1.0)
+    fhat = torch.zeros(9, device=dev)
+    D.project(ctx, torch.tensor(idx, device=dev), fhat)
+    P = synth.param_count(f["C"], f["L"])
+    grad = torch.zeros(P + 1, device=dev)
+    D.project_and_grad(ctx, torch.tensor(idx, device=dev), torch.tensor(y, device=dev), grad)
+    torch.cuda.synchronize()
+    rf, _, rc = O.project(g, th, t, f, B, prm, idx)
+    assert rc == 0 and rel_linf(fhat.cpu().numpy(), rf) <= 1e-5
+    ref, rc = O.project_and_grad(g, th, t, f, B, prm, idx, y)
+    assert max(tensor_errs(grad.cpu().numpy()[:P], ref[:P], f["C"], f["L"])) <= 1e-4
+    with pytest.raises(D.DinrError):
+        D.set_field_weights(ctx, f, torch.tensor(B, device=dev), torch.tensor(prm, device=dev), precision="bf16")

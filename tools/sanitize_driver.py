@@ -45,7 +45,7 @@ def step(name, n, over=None, fover=None, precision="bf16", extra=False):
         gr = D.default_grid(ctx)
         gr = dict(gr, nz=2)
         vox = torch.zeros(gr["nx"] * gr["ny"] * 2, device=dev)
-        D.voxelize(ctx, gr, 0.0, 0, 2, vox)
+        D.voxelize(ctx, gr, 0.0, vox, 0, 2)
     torch.cuda.synchronize()
     st = D.get_device_status(ctx)
     assert st == 0, (st, D.load().dinr_last_error(ctx))
