@@ -222,6 +222,17 @@ size_t plan_layout(dinr_ctx *c, int64_t n, bool train, bool host_io, Plan &pl, v
   static const bool zall_on = std::getenv("DINR_ZALL") != nullptr;
   const bool zall_path = train && !simt && !use_fused(c) && c->H == 256 && fwd3_on() && zall_on;
   if (zall_path) pl.ks0 = pl.ks1 = pl.ksplit = (int)std::max<int64_t>(1, std::min<int64_t>(pl.n_tiles, c->sm_count / c->L));
+  static const bool split_feat0 = std::getenv("DINR_SPLIT_FEAT0") != nullptr;
+  const bool sfeat0 = split_feat0 && !zall_path && train && !simt && !use_fused(c) && c->L >= 2;
+  if (sfeat0) {  // layer-0 CTAs rebuild the features (MUFU): give them w0 x the K-split of the others
+    static const double w0 = std::getenv("DINR_DW_W0") ? std::atof(std::getenv("DINR_DW_W0")) : 2.0;
+    const int sm = c->sm_count / pl.nmb;
+    pl.ks0 = std::max(1, (int)(sm * w0 / (w0 + c->L - 1) + 0.5));
+    pl.ks1 = std::max(1, (sm - pl.ks0) / (c->L - 1));
+    pl.ks0 = (int)std::min<int64_t>(pl.ks0, pl.n_tiles);
+    pl.ks1 = (int)std::min<int64_t>(pl.ks1, pl.n_tiles);
+    pl.ksplit = std::max(pl.ks0, pl.ks1);
+  }
   const int ks = simt ? pl.ksplit_simt : pl.ksplit;
   pl.head_part = ar.take<float>((size_t)std::max(pl.grid_tc, ks) * (H + 1));
   pl.dw_part = pl.db_part = nullptr;
@@ -288,7 +299,8 @@ size_t plan_layout(dinr_ctx *c, int64_t n, bool train, bool host_io, Plan &pl, v
     pl.n_tiles = H == 256 ? 4 * ((pl.nsamp + 511) / 512) : 2 * ((pl.nsamp + 255) / 256);
     // H = 256 with k_tc_fwd3: the forward stashes y = z / 2 of every layer (fp16) and nothing else
     pl.zall = zall_path;
-    pl.feat0 = pl.zall;
+    // layer 0's dW operand (the GRFF features) recomputed by the dW GEMM instead of stashed by K2
+    pl.feat0 = pl.zall || sfeat0;
     if (!pl.zall) pl.hstash = ar.take<uint8_t>((size_t)L * pl.n_tiles * H * 256);
     if (pl.zall) pl.db3 = ar.take<float>((size_t)L * 2 * pl.grid_tc * 128);
     pl.dstash = ar.take<uint8_t>((size_t)L * pl.n_tiles * H * 256);

@@ -14,7 +14,9 @@
 // Work unit: pair-iteration pi = 512 samples = 4 tiles; stream s, CTA rank r owns tile 4 pi + 2 s + r
 // (TMEM lanes = its 128 samples).  Per layer l the leader issues, for (s, h) = (0,0) (0,1) (1,0)
 // (1,1): 16 MMAs M = 256, N = 128 (output features [128 h, 128 h + 128)), K = 256, into TMEM
-// columns [256 s + 128 h, +128) of both CTAs.  Same math, rounding and outputs as k_tc_fwd2 /
+// columns [256 s + 128 h, +128) of both CTAs.  W buffer h holds this CTA's rows of W_l piece h for
+// both streams (loaded once per layer, after stream 1's piece-h MMAs of the previous layer retired),
+// so the next layer's pieces load while stream 1 finishes and stream 0's epilogue runs.  Same math, rounding and outputs as k_tc_fwd2 /
 // k_tc_mlp MODE 1 (ray-chunk sums of M, h_l images to the h stash, swish'(z_l) / z_{L-1} to the
 // s2 stash).
 //   warps 0-7: stream 0 epilogue, warps 8-15: stream 1 (thread = sample row x column half)
@@ -24,7 +26,7 @@
 // Barriers (per CTA unless noted):
 //   w_full[b]   leader only: its own half loaded (expect_tx) + the peer's half loaded (remote arrive)
 //   w_loc[b]    peer only: its own half loaded
-//   w_free[b]   MMAs reading buffer b retired (multicast commit to both CTAs)
+//   w_free[b]   stream 1's MMAs on buffer b retired (multicast commit to both CTAs)
 //   a_full[s]   leader only: A_s written by both CTAs' stream-s epilogues (1 local + 1 remote arrive)
 //   a_rdy[s]    A_s written by this CTA's epilogue (for its stash store thread)
 //   acc_full[s] stream s's layer retired (multicast commit) and this CTA's stash store read A_s
@@ -44,13 +46,27 @@ namespace dinr {
 #define F3_ACC(v) (void)0
 #endif
 
+// Each stream-layer's N = 256 output features run as NP pieces of N = 256 / NP (one pair MMA chain per
+// piece); each CTA holds 128 / NP rows of a piece's W block (this CTA's half), in NWB ring buffers
+// (64 KB in total), so loads run NWB - 1 pieces ahead of the MMAs.  NP = 2 (N = 128, two 32 KB
+// buffers) is the default: NP = 4 (N = 64, four 16 KB buffers, a deeper weight pipeline) measured
+// slower (cone4d2048 forward 5.5 -> 7.4 ms): an M = 256, N = 64 pair MMA reads 5 KB of operands per
+// 32 cycles from each SM's shared memory, above its 128 B/clk.
+#ifndef F3_PIECES
+#define F3_PIECES 2
+#endif
 struct Fwd3Layout {
   static constexpr int H = 256, C = 128;
+  static constexpr int NP = F3_PIECES;             // N pieces per stream-layer
+  static constexpr int NWB = NP;                   // one W buffer per piece (64 KB in total), shared by both streams
+  static constexpr int PN = H / NP;                // N of one piece (pair MMA)
+  static constexpr int PR = PN / 2;                // W rows per CTA per piece
   static constexpr int NT = 512 + 96;
-  static constexpr uint32_t A_BYTES = H * 256u;   // 128 rows x 256 bf16
-  static constexpr uint32_t WQ_BYTES = 64 * 512u;  // this CTA's half of a W_l N-half: 64 rows x 256 K
+  static constexpr uint32_t A_BYTES = H * 256u;    // 128 rows x 256 bf16
+  static constexpr uint32_t WQ_BYTES = PR * 512u;  // this CTA's rows of a piece: PR rows x 256 K
   static size_t smem_bytes(int L) {
-    return 1024 + 2 * (size_t)A_BYTES + 2 * WQ_BYTES + (size_t)L * H * 4 + (H + 4) * 4 + C * 16 + 2 * 2 * 128 * 4 + 256;
+    return 1024 + 2 * (size_t)A_BYTES + NWB * (size_t)WQ_BYTES + (size_t)L * H * 4 + (H + 4) * 4 + C * 16 +
+           2 * 2 * 128 * 4 + 512;
   }
 };
 
@@ -62,24 +78,27 @@ __global__ void __launch_bounds__(Fwd3Layout::NT, 1) k_tc_fwd3(TcParams p) {
   uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // same offsets in both CTAs
   const int L = p.L;
   uint8_t *sA0 = smem;                            // A tiles of streams 0, 1
-  uint8_t *sW = sA0 + 2 * A_BYTES;                // two W buffers: [4 K-blocks][64 rows][128 B]
-  float *sBias = reinterpret_cast<float *>(sW + 2 * WQ);
+  uint8_t *sW = sA0 + 2 * A_BYTES;                // NWB W buffers: [4 K-blocks][PR rows][128 B]
+  float *sBias = reinterpret_cast<float *>(sW + LY::NWB * WQ);
   float *sWo = sBias + L * H;                     // w_o[H], b_o
   float *sB = sWo + H + 4;                        // C x 4
   float *sMu = sB + C * 4;                        // [2 streams][2 column halves][128 rows]
   uint64_t *bars = reinterpret_cast<uint64_t *>(sMu + 2 * 2 * 128);
-  uint64_t *w_full = bars, *w_loc = bars + 2, *w_free = bars + 4;  // [2] each
-  uint64_t *a_full = bars + 6, *a_rdy = bars + 8, *acc_full = bars + 10;  // [2] each
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 12);
+  constexpr int NWB = LY::NWB, NP = LY::NP, PN = LY::PN, PR = LY::PR;
+  uint64_t *w_full = bars, *w_loc = bars + NWB, *w_free = bars + 2 * NWB;  // [NWB] each
+  uint64_t *a_full = bars + 3 * NWB, *a_rdy = a_full + 2, *acc_full = a_full + 4;  // [2] each
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(a_full + 6);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t rank = cluster_ctarank();
   const bool leader = rank == 0;
   if (tid == 512) {
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < NWB; ++i) {
       mbar_init(&w_full[i], 2);
       mbar_init(&w_loc[i], 1);
       mbar_init(&w_free[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
       mbar_init(&a_full[i], 2);
       mbar_init(&a_rdy[i], 1);
       mbar_init(&acc_full[i], 2);
@@ -108,18 +127,19 @@ __global__ void __launch_bounds__(Fwd3Layout::NT, 1) k_tc_fwd3(TcParams p) {
     if (leader) {
       // ============================================================ MMA issue (leader)
       const uint32_t a_base0 = smem_u32(sA0), w_base = smem_u32(sW);
-      const uint32_t idesc = idesc_bf16(256, 128, 0, 0);
+      const uint32_t idesc = idesc_bf16(256, PN, 0, 0);
       uint32_t aph[2] = {0, 0};
-      uint32_t step = 0;
+      uint32_t lay = 0;  // layers processed so far (W buffer phase)
       [[maybe_unused]] unsigned long long ph_w = 0, ph_a = 0;
       for (int64_t pi = cl; pi < n_iter; pi += ncl) {
-        for (int l = 0; l < L; ++l) {
+        for (int l = 0; l < L; ++l, ++lay) {
           for (int s = 0; s < 2; ++s) {
-            for (int h = 0; h < 2; ++h, ++step) {
-              const uint32_t b = step & 1;
-              {
+            for (int h = 0; h < NP; ++h) {
+              // buffer h holds this CTA's rows of W_l piece h for both streams: loaded once per layer,
+              // waited for by stream 0's step, released after stream 1's
+              if (s == 0) {
                 F3_T0();
-                mbar_wait_cluster(&w_full[b], (step >> 1) & 1);
+                mbar_wait_cluster(&w_full[h], lay & 1);
                 F3_ACC(ph_w);
               }
               if (h == 0) {
@@ -129,15 +149,15 @@ __global__ void __launch_bounds__(Fwd3Layout::NT, 1) k_tc_fwd3(TcParams p) {
                 aph[s] ^= 1;
               }
               tc_fence_after();
-              const uint32_t a_base = a_base0 + s * A_BYTES, wb = w_base + b * WQ;
+              const uint32_t a_base = a_base0 + s * A_BYTES, wb = w_base + h * WQ;
 #pragma unroll 4
               for (int kk = 0; kk < H / 16; ++kk) {
                 uint64_t ad = sdesc_sw128(a_base + (kk >> 2) * (128 * 128) + (kk & 3) * 32, 16, 1024);
-                uint64_t bd = sdesc_sw128(wb + (kk >> 2) * 8192 + (kk & 3) * 32, 16, 1024);
-                umma_bf16_pair(tmem + s * 256 + h * 128, ad, bd, idesc, kk > 0 ? 1u : 0u);
+                uint64_t bd = sdesc_sw128(wb + (kk >> 2) * (PR * 128) + (kk & 3) * 32, 16, 1024);
+                umma_bf16_pair(tmem + s * 256 + h * PN, ad, bd, idesc, kk > 0 ? 1u : 0u);
               }
-              umma_commit_pair(&w_free[b], 3);
-              if (h == 1) umma_commit_pair(&acc_full[s], 3);
+              if (s == 1) umma_commit_pair(&w_free[h], 3);
+              if (h == NP - 1) umma_commit_pair(&acc_full[s], 3);
             }
           }
         }
@@ -153,30 +173,27 @@ __global__ void __launch_bounds__(Fwd3Layout::NT, 1) k_tc_fwd3(TcParams p) {
     // ============================================================ W loads (both CTAs)
     const uint8_t *wsrc = reinterpret_cast<const uint8_t *>(p.wpack);
     const uint32_t w_full_leader = mapa_shared(smem_u32(&w_full[0]), 0);
-    uint32_t step = 0;
+    uint32_t lay = 0;
     [[maybe_unused]] unsigned long long ph_lf = 0, ph_ll = 0;
     for (int64_t pi = cl; pi < n_iter; pi += ncl) {
-      for (int l = 0; l < L; ++l) {
-        for (int s = 0; s < 2; ++s) {
-          for (int h = 0; h < 2; ++h, ++step) {
-            const uint32_t b = step & 1;
-            if (step >= 2) {
-              F3_T0();
-              mbar_wait(&w_free[b], ((step >> 1) - 1) & 1);
-              F3_ACC(ph_lf);
-            }
-            uint64_t *bar = leader ? &w_full[b] : &w_loc[b];
-            mbar_arrive_expect_tx(bar, WQ);
-            // this CTA's rows [128 h + 64 r, +64) of every 64-column K-block of the W_l image
-            for (int kb = 0; kb < 4; ++kb)
-              bulk_g2s(sW + b * WQ + kb * 8192, wsrc + (size_t)l * W_LAYER + kb * (H * 128) + (size_t)(128 * h + 64 * rank) * 128,
-                       8192, bar);
-            if (!leader) {
-              F3_T0();
-              mbar_wait(&w_loc[b], (step >> 1) & 1);
-              F3_ACC(ph_ll);
-              mbar_arrive_remote(w_full_leader + b * 8);
-            }
+      for (int l = 0; l < L; ++l, ++lay) {
+        for (int h = 0; h < NP; ++h) {
+          if (lay > 0) {  // stream 1's MMAs on the previous layer's piece h retired
+            F3_T0();
+            mbar_wait(&w_free[h], (lay - 1) & 1);
+            F3_ACC(ph_lf);
+          }
+          uint64_t *bar = leader ? &w_full[h] : &w_loc[h];
+          mbar_arrive_expect_tx(bar, WQ);
+          // this CTA's rows [PN h + PR r, +PR) of every 64-column K-block of the W_l image
+          for (int kb = 0; kb < 4; ++kb)
+            bulk_g2s(sW + h * WQ + kb * (PR * 128),
+                     wsrc + (size_t)l * W_LAYER + kb * (H * 128) + (size_t)(PN * h + PR * rank) * 128, PR * 128, bar);
+          if (!leader) {
+            F3_T0();
+            mbar_wait(&w_loc[h], lay & 1);
+            F3_ACC(ph_ll);
+            mbar_arrive_remote(w_full_leader + h * 8);
           }
         }
       }

@@ -102,7 +102,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_mlp(TcParams p) {
   uint64_t *mma_bar = bars, *w_bar = bars + 2;  // mma_bar[cg]: N-half cg of the current MMA retired
   uint64_t *sa_ok = bars + 3;                    // MODE 1: sA may be rewritten (see the epilogue)
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 4);
-  uint64_t *db_bar = bars + 5;  // (the per-half head partials sMu start after it)
+  uint64_t *db_bar = bars + 5;
+  uint64_t *w_bar1 = bars + 6;  // K3 at H = 256: second half of the streamed W_l (sMu starts after it)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   // K3 on the zall path also accumulates db_l = sum_samples delta_l with a ones-MMA per m-block
@@ -119,6 +120,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_mlp(TcParams p) {
     mbar_init(w_bar, 1);
     mbar_init(sa_ok, 1);
     mbar_init(db_bar, 1);
+    mbar_init(w_bar1, 1);
     fence_mbar_init();
   }
   if (dbm) {
@@ -137,7 +139,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_mlp(TcParams p) {
   const uint32_t tmem_row = tmem + ((uint32_t)((warp & 3) * 32) << 16);
   const int cg = tid >> 7;                     // column half of this thread
   const int cb_lo = cg * (H / 64);  // first of its H/64 32-column chunks
-  float *sMu = reinterpret_cast<float *>(bars + 6);  // [2][128] per-half head partials (forward)
+  float *sMu = reinterpret_cast<float *>(bars + 7);  // [2][128] per-half head partials (forward)
   // the training plan may round the tile count up (paired tiles): padding tiles hold invalid samples
   const int n_tiles = (int)(p.n_tiles > (p.nsamp + 127) / 128 ? p.n_tiles : (p.nsamp + 127) / 128);
 
@@ -162,7 +164,35 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_mlp(TcParams p) {
     }
     return resident ? w_base + (uint32_t)layer * W_LAYER : w_base;
   };
-  if (tid == 0 && (int)blockIdx.x < n_tiles && (!TRAIN || L >= 2)) w_issue(TRAIN ? L - 1 : 0);
+  // K3 streaming H = 256: W_l in two 64 KB halves (the MN-major blocks of input features [128 h,
+  // +128), one per dX MMA half) with their own barriers, so the next layer's half h loads as soon as
+  // this layer's half-h MMA has retired and the next half-0 MMA waits for 64 KB, not 128
+  constexpr bool kHalfW = TRAIN && H == 256;
+  uint32_t wh_phase[2] = {0, 0};
+  bool wh_pending[2] = {false, false};
+  uint64_t *wh_bar[2] = {w_bar, w_bar1};
+  auto wh_issue = [&](int layer, int h) {
+    mbar_arrive_expect_tx(wh_bar[h], W_LAYER / 2);
+    const uint8_t *src = reinterpret_cast<const uint8_t *>(p.wpack) + (size_t)layer * W_LAYER + (size_t)h * (W_LAYER / 2);
+    bulk_g2s(sW + h * (W_LAYER / 2), src, W_LAYER / 4, wh_bar[h]);
+    bulk_g2s(sW + h * (W_LAYER / 2) + W_LAYER / 4, src + W_LAYER / 4, W_LAYER / 4, wh_bar[h]);
+    wh_pending[h] = true;
+  };
+  auto wh_ready = [&](int h) {
+    if (wh_pending[h]) {
+      mbar_wait(wh_bar[h], wh_phase[h]);
+      wh_phase[h] ^= 1;
+      wh_pending[h] = false;
+    }
+  };
+  if (tid == 0 && (int)blockIdx.x < n_tiles && (!TRAIN || L >= 2)) {
+    if (kHalfW && !resident) {
+      wh_issue(L - 1, 0);
+      wh_issue(L - 1, 1);
+    } else {
+      w_issue(TRAIN ? L - 1 : 0);
+    }
+  }
 
   uint32_t mma_phase = 0, sa_phase = 0;
   constexpr int NCB = H / 64;  // 32-column chunks of this thread's column half
@@ -451,14 +481,15 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_mlp(TcParams p) {
               ld_global_v8_hint(zsrc + (size_t)((cb_lo + c) * 2 + qq) * 128 * 32, zq[c][2 * qq], zq[c][2 * qq + 1], pol_z);
         }
         if (tid == 0) {
-          uint32_t wl = w_ready(l);
-          tc_fence_after();
+          uint32_t wl = (kHalfW && !resident) ? w_base : w_ready(l);
           // z of the next step (or the next tile's top layer) into L2 while this step runs
           if (l >= 2)
             bulk_prefetch_l2(p.zstash + ((size_t)(l - 2) * p.n_tiles + tile) * kZTile, kZTile);
           else if (more_tiles)
             bulk_prefetch_l2(p.zstash + ((size_t)(L - 1) * p.n_tiles + tile + gridDim.x) * kZTile, kZTile);
           for (int half = 0; half < 2; ++half) {  // input columns [half NH, (half+1) NH)
+            if (kHalfW && !resident) wh_ready(half);
+            tc_fence_after();
             if (half == 0 || kSplit) {
 #pragma unroll 4
               for (int kk = 0; kk < H / 16; ++kk) {
@@ -474,11 +505,17 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_mlp(TcParams p) {
         mma_phase ^= 1;
         tc_fence_after();
         if (tid == 0) {
-          mbar_wait(&mma_bar[1], mma_phase ^ 1);
-          if (!resident) {  // next: layer l-1, or the next tile's top layer
-            const int nxt = (l - 1 >= 1) ? l - 1 : L - 1;
-            const bool has_next = (l - 1 >= 1) || more_tiles;
-            if (has_next && nxt != w_cur) w_issue(nxt);
+          const int nxt = (l - 1 >= 1) ? l - 1 : L - 1;
+          const bool has_next = (l - 1 >= 1) || more_tiles;
+          if (kHalfW && !resident) {  // half 0 retired (waited above): reload it, then half 1
+            if (has_next) wh_issue(nxt, 0);
+            mbar_wait(&mma_bar[1], mma_phase ^ 1);
+            if (has_next) wh_issue(nxt, 1);
+          } else {
+            mbar_wait(&mma_bar[1], mma_phase ^ 1);
+            if (!resident) {  // next: layer l-1, or the next tile's top layer
+              if (has_next && nxt != w_cur) w_issue(nxt);
+            }
           }
           bulk_wait_read_all();
         }
