@@ -141,6 +141,7 @@ def oracle_rate(name, budget_s=15.0, max_pixels=1 << 20):
     B = synth.grff_matrix(f["C"], f["sigma_t"], f["sigma_s"])
     prm = synth.init_params(f["C"], f["L"])
     S, ns = g["sub_x"] * g["sub_z"], g["n_s"]
+    max_pixels = min(max_pixels, len(th) * g["n_rows"] * g["n_cols"])  # (the whole dataset at most)
     n, last = 1, None
     while n <= max_pixels:
         idx = synth.pixel_batch(name, n, seed=99)

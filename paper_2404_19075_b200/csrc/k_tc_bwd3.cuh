@@ -85,13 +85,14 @@ __global__ void __launch_bounds__(Bwd3Layout::NT, 1) k_tc_bwd3(TcParams p, int n
       const uint32_t a_base0 = smem_u32(sA0), w_base = smem_u32(sW);
       const uint32_t idesc = idesc_bf16(256, 128, 0, 1);  // A K-major (delta rows), B MN-major (W_l)
       uint32_t aph[2] = {0, 0};
-      uint32_t step = 0;
+      uint32_t lay = 0;  // dX layers processed so far (W buffer phase)
       for (int64_t pi = cl; pi < n_iter; pi += ncl) {
-        for (int l = L - 1; l >= 1; --l) {
+        for (int l = L - 1; l >= 1; --l, ++lay) {
           for (int s = 0; s < 2; ++s) {
-            for (int h = 0; h < 2; ++h, ++step) {
-              const uint32_t b = step & 1;
-              mbar_wait_cluster(&w_full[b], (step >> 1) & 1);
+            for (int h = 0; h < 2; ++h) {
+              // buffer h holds this CTA's block of W_l for both streams (loaded once per layer)
+              const uint32_t b = h;
+              if (s == 0) mbar_wait_cluster(&w_full[b], lay & 1);
               if (h == 0) {
                 mbar_wait_cluster(&a_full[s], aph[s]);
                 aph[s] ^= 1;
@@ -104,7 +105,7 @@ __global__ void __launch_bounds__(Bwd3Layout::NT, 1) k_tc_bwd3(TcParams p, int n
                 uint64_t bd = sdesc_sw128(wb + kk * 2048, WQ, 1024);
                 umma_bf16_pair(tmem + s * 256 + h * 128, ad, bd, idesc, kk > 0 ? 1u : 0u);
               }
-              umma_commit_pair(&w_free[b], 3);
+              if (s == 1) umma_commit_pair(&w_free[b], 3);
               if (h == 1) umma_commit_pair(&acc_full[s], 3);
             }
           }
@@ -115,21 +116,19 @@ __global__ void __launch_bounds__(Bwd3Layout::NT, 1) k_tc_bwd3(TcParams p, int n
     // ============================================================ W loads (both CTAs)
     const uint8_t *wsrc = reinterpret_cast<const uint8_t *>(p.wpack);
     const uint32_t w_full_leader = mapa_shared(smem_u32(&w_full[0]), 0);
-    uint32_t step = 0;
+    uint32_t lay = 0;
     for (int64_t pi = cl; pi < n_iter; pi += ncl) {
-      for (int l = L - 1; l >= 1; --l) {
-        for (int s = 0; s < 2; ++s) {
-          for (int h = 0; h < 2; ++h, ++step) {
-            const uint32_t b = step & 1;
-            if (step >= 2) mbar_wait(&w_free[b], ((step >> 1) - 1) & 1);
-            uint64_t *bar = leader ? &w_full[b] : &w_loc[b];
-            mbar_arrive_expect_tx(bar, WQ);
-            // this CTA's 64-column block 2h + r of the MN-major W_l image (input features)
-            bulk_g2s(sW + b * WQ, wsrc + (size_t)l * W_LAYER + (size_t)(2 * h + rank) * WQ, WQ, bar);
-            if (!leader) {
-              mbar_wait(&w_loc[b], (step >> 1) & 1);
-              mbar_arrive_remote(w_full_leader + b * 8);
-            }
+      for (int l = L - 1; l >= 1; --l, ++lay) {
+        for (int h = 0; h < 2; ++h) {
+          const uint32_t b = h;
+          if (lay > 0) mbar_wait(&w_free[b], (lay - 1) & 1);  // stream 1's MMAs on the previous layer's block
+          uint64_t *bar = leader ? &w_full[b] : &w_loc[b];
+          mbar_arrive_expect_tx(bar, WQ);
+          // this CTA's 64-column block 2h + r of the MN-major W_l image (input features)
+          bulk_g2s(sW + b * WQ, wsrc + (size_t)l * W_LAYER + (size_t)(2 * h + rank) * WQ, WQ, bar);
+          if (!leader) {
+            mbar_wait(&w_loc[b], lay & 1);
+            mbar_arrive_remote(w_full_leader + b * 8);
           }
         }
       }
