@@ -437,8 +437,8 @@ dinr_status launch_tc_mlp(dinr_ctx *c, const Plan &pl, int mode, cudaStream_t st
   p.zall = pl.zall ? 1 : 0;
   p.db3 = pl.db3;
   size_t smem = TcLayout<H>::smem_bytes(c->L, p.resident != 0);
-  if (mode == 2 && H == 256 && !pl.zall && std::getenv("DINR_BWD3") && !std::getenv("DINR_BWD2")) {
-    // CTA pairs (cta_group::2, M = 256), two tile streams, W_l blocks double-buffered (k_tc_bwd3.cuh)
+  if (mode == 2 && H == 256 && !pl.zall && fwd3_on() && !std::getenv("DINR_NO_BWD3") && !std::getenv("DINR_BWD2")) {
+    // CTA pairs (cta_group::2, M = 256), two tile streams sharing each W_l block (k_tc_bwd3.cuh)
     const size_t sm3 = Bwd3Layout::smem_bytes();
     dinr_status s = set_smem(c, k_tc_bwd3, sm3);
     if (s) return s;

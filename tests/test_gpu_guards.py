@@ -16,8 +16,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 @pytest.mark.parametrize("part,extra", [("fused", {}), ("split", {}), ("split", {"DINR_ZALL": "1"}),
-                                        ("split", {"DINR_BWD3": "1"}), ("verify", {})],
-                         ids=["fused", "split", "split-zall", "split-bwd3", "verify"])
+                                        ("split", {"DINR_NO_BWD3": "1"}), ("verify", {})],
+                         ids=["fused", "split", "split-zall", "split-k3", "verify"])
 def test_no_out_of_bounds_scratch_writes(part, extra):
     torch = pytest.importorskip("torch")
     if not torch.cuda.is_available():

@@ -5,7 +5,7 @@ fresh process because the library reads its DINR_* path switches once:
   DINR_NO_FUSED  the split path (K2 / K4 / K3 / K5) at H = 128
   DINR_NO_FWD2   the one-tile K2 (k_tc_mlp MODE 1) instead of k_tc_fwd2 at H = 256
   DINR_BWD2      the two-stream K3 experiment k_tc_bwd2 instead of k_tc_mlp MODE 2 at H = 256
-  DINR_BWD3      the CTA-pair K3 experiment k_tc_bwd3
+  DINR_NO_BWD3   the one-tile K3 k_tc_mlp MODE 2 instead of the CTA-pair k_tc_bwd3
   DINR_ZALL      the y-only stash experiment (k_tc_fwd3 zall, k_tc_mlp MODE 3, k_tc_dwz)
   DINR_NO_FWD3   k_tc_fwd2 instead of the CTA-pair K2 k_tc_fwd3
 plus the default paths for reference."""
@@ -32,7 +32,7 @@ CASES = [
     ({}, CONE256, 0),
     ({"DINR_NO_FWD2": "1"}, CONE256, 0),
     ({"DINR_BWD2": "1"}, CONE256, 0),
-    ({"DINR_BWD3": "1"}, CONE256, 0),
+    ({"DINR_NO_BWD3": "1"}, CONE256, 0),
     ({"DINR_ZALL": "1"}, CONE256, 0),
     ({"DINR_NO_FWD3": "1"}, CONE256, 0),
 ]
@@ -45,7 +45,7 @@ def test_path_gradient_parity(env, case, kind):
         pytest.skip("no CUDA device")
     name, over, fover, n = case
     e = dict(os.environ)
-    for k in ("DINR_FUSED_V1", "DINR_NO_DW01", "DINR_NO_FUSED", "DINR_NO_FWD2", "DINR_BWD2", "DINR_BWD3", "DINR_ZALL", "DINR_NO_FWD3"):
+    for k in ("DINR_FUSED_V1", "DINR_NO_DW01", "DINR_NO_FUSED", "DINR_NO_FWD2", "DINR_BWD2", "DINR_NO_BWD3", "DINR_ZALL", "DINR_NO_FWD3"):
         e.pop(k, None)
     e.update(env)
     out = subprocess.run([sys.executable, CHILD, name, json.dumps(over), json.dumps(fover), str(n)], env=e,
