@@ -169,7 +169,12 @@ __global__ void __launch_bounds__(DwzLayout::NT, 1) k_tc_dwz(DwParams p) {
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
               const float2 yf = __half22float2(*reinterpret_cast<const __half2 *>(&yy[e]));
+#ifdef DINR_ZALL_F32_TANH
               w8[e] = pack_bf16x2(fmaf(yf.x, tanh_approx(yf.x), yf.x), fmaf(yf.y, tanh_approx(yf.y), yf.y));
+#else  // one MUFU op for both (bf16x2 tanh: the h it feeds is rounded to bf16 right after)
+              const uint32_t tt = bf2_tanh(pack_bf16x2(yf.x, yf.y));
+              w8[e] = pack_bf16x2(fmaf(yf.x, bf16lo(tt), yf.x), fmaf(yf.y, bf16hi(tt), yf.y));
+#endif
             }
             const int col = e8 * 32 + c * 16;
             st_shared_v4(sb + sw128_offset(r, col, 64), w8[0], w8[1], w8[2], w8[3]);

@@ -536,7 +536,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_mlp(TcParams p) {
               float s0, s1;
               if (ZALL) {  // swish'(z) from the stashed y = z / 2: s = (1 + tanh y) / 2, s (1 + 2 y (1 - s))
                 const float2 yf = __half22float2(*reinterpret_cast<const __half2 *>(&zz[e]));
+#ifdef DINR_ZALL_F32_TANH
                 const float g0 = fmaf(0.5f, tanh_approx(yf.x), 0.5f), g1 = fmaf(0.5f, tanh_approx(yf.y), 0.5f);
+#else  // bf16x2 tanh, one MUFU op for both: the same precision as the bf16 swish' stash of the default path
+                const uint32_t tt = bf2_tanh(pack_bf16x2(yf.x, yf.y));
+                const float g0 = fmaf(0.5f, bf16lo(tt), 0.5f), g1 = fmaf(0.5f, bf16hi(tt), 0.5f);
+#endif
                 s0 = fmaf(g0, 2.f * yf.x * (1.f - g0), g0);
                 s1 = fmaf(g1, 2.f * yf.y * (1.f - g1), g1);
               } else {
