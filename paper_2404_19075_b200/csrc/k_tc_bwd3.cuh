@@ -121,13 +121,13 @@ __global__ void __launch_bounds__(Bwd3Layout::NT, 1) k_tc_bwd3(TcParams p, int n
       for (int l = L - 1; l >= 1; --l, ++lay) {
         for (int h = 0; h < 2; ++h) {
           const uint32_t b = h;
-          if (lay > 0) mbar_wait(&w_free[b], (lay - 1) & 1);  // stream 1's MMAs on the previous layer's block
+          if (lay > 0) mbar_wait_long(&w_free[b], (lay - 1) & 1);  // stream 1's MMAs on the previous layer's block
           uint64_t *bar = leader ? &w_full[b] : &w_loc[b];
           mbar_arrive_expect_tx(bar, WQ);
           // this CTA's 64-column block 2h + r of the MN-major W_l image (input features)
           bulk_g2s(sW + b * WQ, wsrc + (size_t)l * W_LAYER + (size_t)(2 * h + rank) * WQ, WQ, bar);
           if (!leader) {
-            mbar_wait(&w_loc[b], lay & 1);
+            mbar_wait_long(&w_loc[b], lay & 1);
             mbar_arrive_remote(w_full_leader + b * 8);
           }
         }
@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(Bwd3Layout::NT, 1) k_tc_bwd3(TcParams p, int n
     for (int64_t pi = cl; pi < n_iter; pi += ncl) {
       for (int l = L - 1; l >= 0; --l) {
         for (int s = 0; s < 2; ++s) {
-          mbar_wait(&a_rdy[s], rph[s]);
+          mbar_wait_long(&a_rdy[s], rph[s]);
           rph[s] ^= 1;
           const int64_t tile = 4 * pi + 2 * s + rank;
           bulk_s2g(p.dstash + ((size_t)l * p.n_tiles + tile) * A_BYTES, sA0 + s * A_BYTES, A_BYTES);
@@ -188,7 +188,7 @@ __global__ void __launch_bounds__(Bwd3Layout::NT, 1) k_tc_bwd3(TcParams p, int n
         uint4 zt[2][2];
         ld_global_v8_hint(zsrc + (size_t)(cb_lo * 2) * 128 * 32, zt[0][0], zt[0][1], pol_z);
         if (a_busy) {
-          mbar_wait(&acc_full[s], accph);  // CTA scope: TMEM + own smem only
+          mbar_wait_long(&acc_full[s], accph);  // CTA scope: TMEM + own smem only
           accph ^= 1;
         }
         a_busy = true;
@@ -252,7 +252,7 @@ __global__ void __launch_bounds__(Bwd3Layout::NT, 1) k_tc_bwd3(TcParams p, int n
         if (l >= 2 && cg == 0 && (row & 31) == 0)  // the next step's state into L2 meanwhile
           bulk_prefetch_l2(p.zstash + ((size_t)(l - 2) * p.n_tiles + tile) * kZTile + (size_t)(row >> 5) * (kZTile / 4),
                            kZTile / 4);
-        mbar_wait(&acc_full[s], accph);  // CTA scope: TMEM + own smem only
+        mbar_wait_long(&acc_full[s], accph);  // CTA scope: TMEM + own smem only
         accph ^= 1;
         tc_fence_after();
 #pragma unroll
@@ -281,7 +281,7 @@ __global__ void __launch_bounds__(Bwd3Layout::NT, 1) k_tc_bwd3(TcParams p, int n
       }
     }
     if (a_busy) {  // the last delta_0 store has read A_s
-      mbar_wait(&acc_full[s], accph);  // CTA scope: TMEM + own smem only
+      mbar_wait_long(&acc_full[s], accph);  // CTA scope: TMEM + own smem only
       accph ^= 1;
     }
   }

@@ -180,7 +180,7 @@ __global__ void __launch_bounds__(Fwd3Layout::NT, 1) k_tc_fwd3(TcParams p) {
         for (int h = 0; h < NP; ++h) {
           if (lay > 0) {  // stream 1's MMAs on the previous layer's piece h retired
             F3_T0();
-            mbar_wait(&w_free[h], (lay - 1) & 1);
+            mbar_wait_long(&w_free[h], (lay - 1) & 1);
             F3_ACC(ph_lf);
           }
           uint64_t *bar = leader ? &w_full[h] : &w_loc[h];
@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(Fwd3Layout::NT, 1) k_tc_fwd3(TcParams p) {
                      wsrc + (size_t)l * W_LAYER + kb * (H * 128) + (size_t)(PN * h + PR * rank) * 128, PR * 128, bar);
           if (!leader) {
             F3_T0();
-            mbar_wait(&w_loc[h], lay & 1);
+            mbar_wait_long(&w_loc[h], lay & 1);
             F3_ACC(ph_ll);
             mbar_arrive_remote(w_full_leader + h * 8);
           }
@@ -213,7 +213,7 @@ __global__ void __launch_bounds__(Fwd3Layout::NT, 1) k_tc_fwd3(TcParams p) {
         for (int s = 0; s < 2; ++s) {
           {
             F3_T0();
-            mbar_wait(&a_rdy[s], rph[s]);
+            mbar_wait_long(&a_rdy[s], rph[s]);
             F3_ACC(ph_sa);
           }
           rph[s] ^= 1;
@@ -308,7 +308,7 @@ __global__ void __launch_bounds__(Fwd3Layout::NT, 1) k_tc_fwd3(TcParams p) {
         const bool last = (l == L - 1);
         {
           F3_T0();
-          mbar_wait(&acc_full[s], accph);  // CTA scope: TMEM + own smem only
+          mbar_wait_long(&acc_full[s], accph);  // CTA scope: TMEM + own smem only
           F3_ACC(ph_e[1]);
         }
         accph ^= 1;

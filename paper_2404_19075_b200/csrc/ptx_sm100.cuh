@@ -89,6 +89,16 @@ __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
+// Long waits of the pair kernels (epilogue on its accumulator, loader / store threads): with
+// DINR_SLEEP_WAITS the waiting thread is suspended in hardware instead of re-issuing the probe.
+__device__ __forceinline__ void mbar_wait_long(uint64_t *bar, uint32_t parity) {
+#ifdef DINR_SLEEP_WAITS
+  mbar_wait_sleep(bar, parity, 2000);
+#else
+  mbar_wait(bar, parity);
+#endif
+}
+
 // ------------------------------------------------------------------ bulk async copies
 // global -> shared, completion signalled on `bar` as transaction bytes.
 __device__ __forceinline__ void bulk_g2s(void *smem_dst, const void *gsrc, uint32_t bytes, uint64_t *bar) {
