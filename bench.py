@@ -55,22 +55,22 @@ def peaks():
 
 
 def profiled_traffic(workload, kernel_class, path_kind):
-    """DRAM bytes per launch of the dominant kernel from the committed ncu --set full capture
-    (profiles/traffic.json, written by tools/ncu_summary.py traffic), or None if that capture is
-    not for this workload / kernel."""
-    names = {"backward": {0: "k_tc_mlp", 1: "k_fused<", 2: "k_fused2<"}.get(path_kind, ""), "dw": "k_tc_dw",
-             "forward": "k_tc_fwd", "rays": "k_ray_setup", "loss": "k_loss"}
+    """DRAM bytes per launch of the dominant kernel from the committed ncu --set full captures
+    (profiles/traffic.json, one entry per workload, written by tools/ncu_summary.py traffic), or
+    None if no capture holds this workload / kernel."""
+    names = {"backward": {0: ("k_tc_bwd", "k_tc_mlp"), 1: ("k_fused<",), 2: ("k_fused2<",)}.get(path_kind, ()),
+             "dw": ("k_tc_dw", "k_dw01"), "forward": ("k_tc_fwd", "k_tc_mlp"), "rays": ("k_ray_setup",),
+             "loss": ("k_loss",)}
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
             tr = json.load(fh)
     except Exception:
         return None
-    if tr.get("workload") != workload:
-        return None
-    want = names.get(kernel_class, "?")
-    for k, v in tr.get("kernels", {}).items():
-        if want and want in k:
-            return v
+    kern = tr.get("workloads", {}).get(workload, {}).get("kernels", {})
+    for want in names.get(kernel_class, ()):  # the first candidate the capture holds
+        for k, v in kern.items():
+            if want in k:
+                return v
     return None
 
 

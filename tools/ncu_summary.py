@@ -82,11 +82,16 @@ def traffic(*args):
             for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
                 tot += float(r[col[m]].replace(",", "")) * scale.get(units[col[m]], 1)
             kern[name] = tot
-    res = {"workload": workload, "source": [os.path.basename(p) for p in paths], "kernels": kern}
     dst = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "traffic.json")
+    try:  # one entry per workload; other workloads' captures are kept
+        with open(dst) as fh:
+            allw = json.load(fh).get("workloads", {})
+    except Exception:
+        allw = {}
+    allw[workload] = {"source": [os.path.basename(p) for p in paths], "kernels": kern}
     with open(dst, "w") as fh:
-        json.dump(res, fh, indent=1)
-    print(json.dumps(res, indent=1))
+        json.dump({"workloads": allw}, fh, indent=1)
+    print(json.dumps(allw[workload], indent=1))
 
 
 if __name__ == "__main__":
