@@ -79,7 +79,7 @@ class ClockSampler:
     """Polls nvidia-smi (one query every ~200 ms) in a background thread."""
     FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
               "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
-              "clocks_event_reasons.sw_power_cap"]
+              "clocks_event_reasons.sw_power_cap", "power.draw", "power.limit"]
     NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, device_index):
@@ -115,18 +115,24 @@ class ClockSampler:
         if self.window:
             w = [r for r in rows if self.window[0] <= r[0] <= self.window[1]]
             rows = w if w else rows
-        sm, mx, reasons = [], [], set()
+        sm, mx, pw, lim, reasons = [], [], [], [], set()
         for _, parts in rows:
             try:
                 sm.append(float(parts[0]))
                 mx.append(float(parts[1]))
             except ValueError:
                 continue
-            for flag, name in zip(parts[2:], self.NAMES):
+            for flag, name in zip(parts[2:6], self.NAMES):
                 if flag.lower() == "active":
                     reasons.add(name)
+            try:
+                pw.append(float(parts[6]))
+                lim.append(float(parts[7]))
+            except (ValueError, IndexError):
+                pass
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm),
+                "power_w": statistics.median(pw) if pw else None, "power_limit_w": max(lim) if lim else None}
 
 
 # ---------------------------------------------------------------------------- oracle timing

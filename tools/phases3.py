@@ -11,7 +11,7 @@ from paper_2404_19075_b200 import _lib as D  # noqa: E402
 from paper_2404_19075_b200 import synth  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "cone4d2048"
-D.load(os.path.join(ROOT, "paper_2404_19075_b200", "libdinr_phases.so"))
+D.load(os.path.join(ROOT, "paper_2404_19075_b200", os.environ.get("DINR_PHASES_LIB", "libdinr_phases.so")))
 dev = torch.device("cuda", 0)
 g = synth.geometry(name)
 th, t = synth.views(name)

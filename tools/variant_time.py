@@ -34,7 +34,16 @@ for _ in range(10):
     a.record(); D.project_and_grad(ctx, idx, y, grad); b.record(); torch.cuda.synchronize()
     ts.append(a.elapsed_time(b))
 ts.sort()
-print(f"{LIB:40s} median {ts[len(ts)//2]:.3f} ms  min {ts[0]:.3f} ms  loss {grad[-1].item():.6f}")
+D.set_timing(ctx, True)
+for k in D.TIMERS:
+    D.read_timing(ctx, k, reset=True)
+for _ in range(5):
+    flush.fill_(1)
+    D.project_and_grad(ctx, idx, y, grad)
+torch.cuda.synchronize()
+D.set_timing(ctx, False)
+kt = " ".join(f"{k} {D.read_timing(ctx, k, reset=True)[0] / 5:.2f}" for k in ("forward", "backward", "dw"))
+print(f"{LIB:40s} median {ts[len(ts)//2]:.3f} ms  min {ts[0]:.3f} ms  loss {grad[-1].item():.6f}  [{kt}]")
 """
 
 if __name__ == "__main__":
