@@ -23,6 +23,7 @@
 //   warp 16 lane 0: MMA issue (leader CTA only)
 //   warp 17 lane 0: W loads of this CTA's half (both CTAs)
 //   warp 18 lane 0: h-stash bulk stores of this CTA's tiles (both CTAs)
+//   warp 19 lane 0: (peer) passes its landed W K-halves on to the leader's w_full
 // Barriers (per CTA unless noted):
 //   w_full[b]   leader only: its own half loaded (expect_tx) + the peer's half loaded (remote arrive)
 //   w_loc[b]    peer only: its own half loaded
@@ -55,15 +56,23 @@ namespace dinr {
 #ifndef F3_PIECES
 #define F3_PIECES 2
 #endif
+// The W pieces move through a ring of F3_WRING K-half buffers (this CTA's rows of a piece for 128 of
+// the 256 K, 16 KB): K-half j of the kernel's sequence (layer-major, piece, K-half; both streams use
+// it) in buffer j mod F3_WRING.  Five buffers (80 KB) let the next layer's first K-half load while
+// the current layer runs; two whole-piece buffers (64 KB) made the MMA wait ~2.4 K cycles per layer
+// for weights that could only start loading after stream 1's MMAs on the previous layer retired.
+#ifndef F3_WRING
+#define F3_WRING 5
+#endif
 struct Fwd3Layout {
   static constexpr int H = 256, C = 128;
   static constexpr int NP = F3_PIECES;             // N pieces per stream-layer
-  static constexpr int NWB = NP;                   // one W buffer per piece (64 KB in total), shared by both streams
+  static constexpr int NWB = F3_WRING;             // K-half W buffers, shared by both streams
   static constexpr int PN = H / NP;                // N of one piece (pair MMA)
   static constexpr int PR = PN / 2;                // W rows per CTA per piece
-  static constexpr int NT = 512 + 96;
+  static constexpr int NT = 512 + 128;
   static constexpr uint32_t A_BYTES = H * 256u;    // 128 rows x 256 bf16
-  static constexpr uint32_t WQ_BYTES = PR * 512u;  // this CTA's rows of a piece: PR rows x 256 K
+  static constexpr uint32_t WQ_BYTES = PR * 256u;  // this CTA's rows of a piece for one K-half: PR rows x 128 K
   static size_t smem_bytes(int L) {
     return 1024 + 2 * (size_t)A_BYTES + NWB * (size_t)WQ_BYTES + (size_t)L * H * 4 + (H + 4) * 4 + C * 16 +
            2 * 2 * 128 * 4 + 512;
@@ -135,28 +144,33 @@ __global__ void __launch_bounds__(Fwd3Layout::NT, 1) k_tc_fwd3(TcParams p) {
         for (int l = 0; l < L; ++l, ++lay) {
           for (int s = 0; s < 2; ++s) {
             for (int h = 0; h < NP; ++h) {
-              // buffer h holds this CTA's rows of W_l piece h for both streams: loaded once per layer,
-              // waited for by stream 0's step, released after stream 1's
-              if (s == 0) {
-                F3_T0();
-                mbar_wait_cluster(&w_full[h], lay & 1);
-                F3_ACC(ph_w);
-              }
+              // K-halves j0, j0 + 1 of piece h (for both streams): waited for by stream 0's step,
+              // released after stream 1's
+              const uint32_t j0 = (lay * NP + h) * 2;
               if (h == 0) {
                 F3_T0();
                 mbar_wait_cluster(&a_full[s], aph[s]);
                 F3_ACC(ph_a);
                 aph[s] ^= 1;
               }
-              tc_fence_after();
-              const uint32_t a_base = a_base0 + s * A_BYTES, wb = w_base + h * WQ;
+              const uint32_t a_base = a_base0 + s * A_BYTES;
+              for (int kh = 0; kh < 2; ++kh) {
+                const uint32_t j = j0 + kh, b = j % NWB;
+                if (s == 0) {
+                  F3_T0();
+                  mbar_wait_cluster(&w_full[b], (j / NWB) & 1);
+                  F3_ACC(ph_w);
+                }
+                tc_fence_after();
+                const uint32_t wb = w_base + b * WQ;
 #pragma unroll 4
-              for (int kk = 0; kk < H / 16; ++kk) {
-                uint64_t ad = sdesc_sw128(a_base + (kk >> 2) * (128 * 128) + (kk & 3) * 32, 16, 1024);
-                uint64_t bd = sdesc_sw128(wb + (kk >> 2) * (PR * 128) + (kk & 3) * 32, 16, 1024);
-                umma_bf16_pair(tmem + s * 256 + h * PN, ad, bd, idesc, kk > 0 ? 1u : 0u);
+                for (int kk = 8 * kh; kk < 8 * kh + 8; ++kk) {
+                  uint64_t ad = sdesc_sw128(a_base + (kk >> 2) * (128 * 128) + (kk & 3) * 32, 16, 1024);
+                  uint64_t bd = sdesc_sw128(wb + ((kk >> 2) & 1) * (PR * 128) + (kk & 3) * 32, 16, 1024);
+                  umma_bf16_pair(tmem + s * 256 + h * PN, ad, bd, idesc, kk > 0 ? 1u : 0u);
+                }
+                if (s == 1) umma_commit_pair(&w_free[b], 3);
               }
-              if (s == 1) umma_commit_pair(&w_free[h], 3);
               if (h == NP - 1) umma_commit_pair(&acc_full[s], 3);
             }
           }
@@ -172,38 +186,52 @@ __global__ void __launch_bounds__(Fwd3Layout::NT, 1) k_tc_fwd3(TcParams p) {
   } else if (tid == 544) {
     // ============================================================ W loads (both CTAs)
     const uint8_t *wsrc = reinterpret_cast<const uint8_t *>(p.wpack);
-    const uint32_t w_full_leader = mapa_shared(smem_u32(&w_full[0]), 0);
     uint32_t lay = 0;
-    [[maybe_unused]] unsigned long long ph_lf = 0, ph_ll = 0;
+    [[maybe_unused]] unsigned long long ph_lf = 0;
     for (int64_t pi = cl; pi < n_iter; pi += ncl) {
       for (int l = 0; l < L; ++l, ++lay) {
         for (int h = 0; h < NP; ++h) {
-          if (lay > 0) {  // stream 1's MMAs on the previous layer's piece h retired
-            F3_T0();
-            mbar_wait_long(&w_free[h], (lay - 1) & 1);
-            F3_ACC(ph_lf);
-          }
-          uint64_t *bar = leader ? &w_full[h] : &w_loc[h];
-          mbar_arrive_expect_tx(bar, WQ);
-          // this CTA's rows [PN h + PR r, +PR) of every 64-column K-block of the W_l image
-          for (int kb = 0; kb < 4; ++kb)
-            bulk_g2s(sW + h * WQ + kb * (PR * 128),
-                     wsrc + (size_t)l * W_LAYER + kb * (H * 128) + (size_t)(PN * h + PR * rank) * 128, PR * 128, bar);
-          if (!leader) {
-            F3_T0();
-            mbar_wait_long(&w_loc[h], lay & 1);
-            F3_ACC(ph_ll);
-            mbar_arrive_remote(w_full_leader + h * 8);
+          for (int kh = 0; kh < 2; ++kh) {
+            const uint32_t j = (lay * NP + h) * 2 + kh, b = j % NWB;
+            if (j >= NWB) {  // stream 1's MMAs on K-half j - NWB (this buffer's last use) retired
+              F3_T0();
+              mbar_wait_long(&w_free[b], ((j / NWB) - 1) & 1);
+              F3_ACC(ph_lf);
+            }
+            uint64_t *bar = leader ? &w_full[b] : &w_loc[b];
+            mbar_arrive_expect_tx(bar, WQ);
+            // this CTA's rows [PN h + PR r, +PR) of 64-column K-blocks 2 kh, 2 kh + 1 of the W_l image
+            for (int q = 0; q < 2; ++q)
+              bulk_g2s(sW + b * WQ + q * (PR * 128),
+                       wsrc + (size_t)l * W_LAYER + (2 * kh + q) * (H * 128) + (size_t)(PN * h + PR * rank) * 128,
+                       PR * 128, bar);
           }
         }
       }
     }
 #ifdef DINR_PHASES
-    if (p.dbg) {
-      p.dbg[(size_t)blockIdx.x * 32 + 10] = ph_lf;
-      p.dbg[(size_t)blockIdx.x * 32 + 11] = ph_ll;
-    }
+    if (p.dbg) p.dbg[(size_t)blockIdx.x * 32 + 10] = ph_lf;
 #endif
+  } else if (tid == 608) {
+    // ============================================================ peer: W halves landed -> leader
+    // (a thread of its own, so the peer's loader keeps loads in flight like the leader's)
+    if (!leader) {
+      const uint32_t w_full_leader = mapa_shared(smem_u32(&w_full[0]), 0);
+      uint32_t lay = 0;
+      [[maybe_unused]] unsigned long long ph_ll = 0;
+      for (int64_t pi = cl; pi < n_iter; pi += ncl)
+        for (int l = 0; l < L; ++l, ++lay)
+          for (uint32_t j = lay * NP * 2; j < (lay + 1) * NP * 2; ++j) {
+            const uint32_t b = j % NWB;
+            F3_T0();
+            mbar_wait_long(&w_loc[b], (j / NWB) & 1);
+            F3_ACC(ph_ll);
+            mbar_arrive_remote(w_full_leader + b * 8);
+          }
+#ifdef DINR_PHASES
+      if (p.dbg) p.dbg[(size_t)blockIdx.x * 32 + 11] = ph_ll;
+#endif
+    }
   } else if (tid == 576) {
     // ============================================================ h-stash stores (both CTAs)
     uint32_t rph[2] = {0, 0};
