@@ -11,6 +11,7 @@
 // delta_l image bulk-stored to the delta stash for the dW GEMM (k_tc_dw.cuh).
 //   warps 0-7: stream 0 epilogue, warps 8-15: stream 1 (thread = sample row x column half)
 //   warp 16 lane 0: MMA issue (leader)     warp 17 lane 0: W loads     warp 18 lane 0: delta stores
+//   warp 19 lane 0: (peer) passes its landed W K-halves on to the leader's w_full
 // Barriers as in k_tc_fwd3; acc_full[s] = the stream's dX MMAs retired + this CTA's delta store
 // read A_s (the store thread arrives twice after delta_0, which no MMA follows).
 #pragma once
@@ -20,40 +21,54 @@
 
 namespace dinr {
 
+// The W blocks move through a ring of B3_WRING K-half buffers (rows [128 kh, +128) of this CTA's
+// 64-column block of piece h, 16 KB): K-half j of the kernel's sequence (layer, piece, K-half; both
+// streams use it) in buffer j mod B3_WRING, so the next layer's first K-half loads while the
+// current layer runs (as k_tc_fwd3).
+#ifndef B3_WRING
+#define B3_WRING 5
+#endif
 struct Bwd3Layout {
   static constexpr int H = 256;
-  static constexpr int NT = 512 + 96;
+  static constexpr int NT = 512 + 128;
+  static constexpr int NWB = B3_WRING;
   static constexpr uint32_t A_BYTES = H * 256u;   // 128 rows x 256 bf16
   static constexpr uint32_t WQ_BYTES = H * 128u;  // one 64-column block of W_l: 256 rows x 128 B
-  static size_t smem_bytes() { return 1024 + 2 * (size_t)A_BYTES + 2 * WQ_BYTES + (H + 4) * 4 + 2 * 8 * (H + 1) * 4 + 256; }
+  static constexpr uint32_t WH_BYTES = WQ_BYTES / 2;  // one K-half of it
+  static size_t smem_bytes() {
+    return 1024 + 2 * (size_t)A_BYTES + NWB * (size_t)WH_BYTES + (H + 4) * 4 + 2 * 8 * (H + 1) * 4 + 256;
+  }
 };
 
 __global__ void __launch_bounds__(Bwd3Layout::NT, 1) k_tc_bwd3(TcParams p, int nhead_slots) {
   using LY = Bwd3Layout;
   constexpr int H = LY::H;
-  constexpr uint32_t A_BYTES = LY::A_BYTES, W_LAYER = H * H * 2u, WQ = LY::WQ_BYTES;
+  constexpr uint32_t A_BYTES = LY::A_BYTES, W_LAYER = H * H * 2u, WQ = LY::WQ_BYTES, WH = LY::WH_BYTES;
+  constexpr int NWB = LY::NWB;
   constexpr int NCB = H / 64;                 // 32-column chunks of a thread's column half
   constexpr uint32_t kZTile = 128u * H * 2u;  // one tile of the 16-bit backward state
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // same offsets in both CTAs
   const int L = p.L;
   uint8_t *sA0 = smem;                              // A tiles (delta_l images) of streams 0, 1
-  uint8_t *sW = sA0 + 2 * A_BYTES;                  // two W buffers: [256 output rows][128 B]
-  float *sWo = reinterpret_cast<float *>(sW + 2 * WQ);  // w_o[H], b_o
+  uint8_t *sW = sA0 + 2 * A_BYTES;                  // NWB W K-half buffers: [128 output rows][128 B]
+  float *sWo = reinterpret_cast<float *>(sW + NWB * WH);  // w_o[H], b_o
   float *red = sWo + H + 4;                          // [16 warps][H + 1] head partials
   uint64_t *bars = reinterpret_cast<uint64_t *>(red + 2 * 8 * (H + 1));
-  uint64_t *w_full = bars, *w_loc = bars + 2, *w_free = bars + 4;
-  uint64_t *a_full = bars + 6, *a_rdy = bars + 8, *acc_full = bars + 10;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 12);
+  uint64_t *w_full = bars, *w_loc = bars + NWB, *w_free = bars + 2 * NWB;  // [NWB] each
+  uint64_t *a_full = bars + 3 * NWB, *a_rdy = a_full + 2, *acc_full = a_full + 4;  // [2] each
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(a_full + 6);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t rank = cluster_ctarank();
   const bool leader = rank == 0;
   if (tid == 512) {
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < NWB; ++i) {
       mbar_init(&w_full[i], 2);
       mbar_init(&w_loc[i], 1);
       mbar_init(&w_free[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
       mbar_init(&a_full[i], 2);
       mbar_init(&a_rdy[i], 1);
       mbar_init(&acc_full[i], 2);
@@ -90,22 +105,26 @@ __global__ void __launch_bounds__(Bwd3Layout::NT, 1) k_tc_bwd3(TcParams p, int n
         for (int l = L - 1; l >= 1; --l, ++lay) {
           for (int s = 0; s < 2; ++s) {
             for (int h = 0; h < 2; ++h) {
-              // buffer h holds this CTA's block of W_l for both streams (loaded once per layer)
-              const uint32_t b = h;
-              if (s == 0) mbar_wait_cluster(&w_full[b], lay & 1);
+              // K-halves of this CTA's block of W_l piece h (for both streams): waited for by stream
+              // 0's step, released after stream 1's
               if (h == 0) {
                 mbar_wait_cluster(&a_full[s], aph[s]);
                 aph[s] ^= 1;
               }
-              tc_fence_after();
-              const uint32_t a_base = a_base0 + s * A_BYTES, wb = w_base + b * WQ;
+              const uint32_t a_base = a_base0 + s * A_BYTES;
+              for (int kh = 0; kh < 2; ++kh) {
+                const uint32_t j = (lay * 2 + h) * 2 + kh, b = j % NWB;
+                if (s == 0) mbar_wait_cluster(&w_full[b], (j / NWB) & 1);
+                tc_fence_after();
+                const uint32_t wb = w_base + b * WH;
 #pragma unroll 4
-              for (int kk = 0; kk < H / 16; ++kk) {  // K = the layer's output features (16 rows of W_l)
-                uint64_t ad = sdesc_sw128(a_base + (kk >> 2) * (128 * 128) + (kk & 3) * 32, 16, 1024);
-                uint64_t bd = sdesc_sw128(wb + kk * 2048, WQ, 1024);
-                umma_bf16_pair(tmem + s * 256 + h * 128, ad, bd, idesc, kk > 0 ? 1u : 0u);
+                for (int kk = 8 * kh; kk < 8 * kh + 8; ++kk) {  // K = the layer's output features (16 rows of W_l)
+                  uint64_t ad = sdesc_sw128(a_base + (kk >> 2) * (128 * 128) + (kk & 3) * 32, 16, 1024);
+                  uint64_t bd = sdesc_sw128(wb + (kk - 8 * kh) * 2048, WH, 1024);
+                  umma_bf16_pair(tmem + s * 256 + h * 128, ad, bd, idesc, kk > 0 ? 1u : 0u);
+                }
+                if (s == 1) umma_commit_pair(&w_free[b], 3);
               }
-              if (s == 1) umma_commit_pair(&w_free[b], 3);
               if (h == 1) umma_commit_pair(&acc_full[s], 3);
             }
           }
@@ -115,23 +134,33 @@ __global__ void __launch_bounds__(Bwd3Layout::NT, 1) k_tc_bwd3(TcParams p, int n
   } else if (tid == 544) {
     // ============================================================ W loads (both CTAs)
     const uint8_t *wsrc = reinterpret_cast<const uint8_t *>(p.wpack);
-    const uint32_t w_full_leader = mapa_shared(smem_u32(&w_full[0]), 0);
     uint32_t lay = 0;
     for (int64_t pi = cl; pi < n_iter; pi += ncl) {
       for (int l = L - 1; l >= 1; --l, ++lay) {
         for (int h = 0; h < 2; ++h) {
-          const uint32_t b = h;
-          if (lay > 0) mbar_wait_long(&w_free[b], (lay - 1) & 1);  // stream 1's MMAs on the previous layer's block
-          uint64_t *bar = leader ? &w_full[b] : &w_loc[b];
-          mbar_arrive_expect_tx(bar, WQ);
-          // this CTA's 64-column block 2h + r of the MN-major W_l image (input features)
-          bulk_g2s(sW + b * WQ, wsrc + (size_t)l * W_LAYER + (size_t)(2 * h + rank) * WQ, WQ, bar);
-          if (!leader) {
-            mbar_wait_long(&w_loc[b], lay & 1);
-            mbar_arrive_remote(w_full_leader + b * 8);
+          for (int kh = 0; kh < 2; ++kh) {
+            const uint32_t j = (lay * 2 + h) * 2 + kh, b = j % NWB;
+            if (j >= NWB) mbar_wait_long(&w_free[b], ((j / NWB) - 1) & 1);  // stream 1's MMAs on K-half j - NWB
+            uint64_t *bar = leader ? &w_full[b] : &w_loc[b];
+            mbar_arrive_expect_tx(bar, WH);
+            // rows [128 kh, +128) of this CTA's 64-column block 2h + r of the MN-major W_l image
+            bulk_g2s(sW + b * WH, wsrc + (size_t)l * W_LAYER + (size_t)(2 * h + rank) * WQ + kh * WH, WH, bar);
           }
         }
       }
+    }
+  } else if (tid == 608) {
+    // ============================================================ peer: W halves landed -> leader
+    if (!leader) {
+      const uint32_t w_full_leader = mapa_shared(smem_u32(&w_full[0]), 0);
+      uint32_t lay = 0;
+      for (int64_t pi = cl; pi < n_iter; pi += ncl)
+        for (int l = L - 1; l >= 1; --l, ++lay)
+          for (uint32_t j = lay * 4; j < lay * 4 + 4; ++j) {
+            const uint32_t b = j % NWB;
+            mbar_wait_long(&w_loc[b], (j / NWB) & 1);
+            mbar_arrive_remote(w_full_leader + b * 8);
+          }
     }
   } else if (tid == 576) {
     // ============================================================ delta-stash stores (both CTAs)
@@ -142,9 +171,11 @@ __global__ void __launch_bounds__(Bwd3Layout::NT, 1) k_tc_bwd3(TcParams p, int n
           mbar_wait_long(&a_rdy[s], rph[s]);
           rph[s] ^= 1;
           const int64_t tile = 4 * pi + 2 * s + rank;
+#ifndef DINR_DBG_K3_NOSTORE  // timing experiment only (the dW GEMM then reads a stale delta stash)
           bulk_s2g(p.dstash + ((size_t)l * p.n_tiles + tile) * A_BYTES, sA0 + s * A_BYTES, A_BYTES);
           bulk_commit();
           bulk_wait_read_all();
+#endif
           mbar_arrive(&acc_full[s]);
           if (l == 0) mbar_arrive(&acc_full[s]);  // no MMA follows delta_0
         }
@@ -247,6 +278,11 @@ __global__ void __launch_bounds__(Bwd3Layout::NT, 1) k_tc_bwd3(TcParams p, int n
       for (int l = L - 1; l >= 1; --l) {
         const uint8_t *zsrc = p.zstash + (((size_t)(l - 1) * p.n_tiles + tile) * (H / 16) * 128 + row) * 32;
         uint4 zq[2 * NCB][2];
+#ifdef DINR_DBG_K3_NOLOAD  // timing experiment only (swish' = 1)
+#pragma unroll
+        for (int k = 0; k < 2 * NCB; ++k) zq[k][0] = zq[k][1] = make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);
+#define ld_global_v8_hint(...) (void)0
+#endif
 #pragma unroll
         for (int k = 0; k < NCB; ++k) ld_global_v8_hint(zsrc + (size_t)(cb_lo * 2 + k) * 128 * 32, zq[k][0], zq[k][1], pol_z);
         if (l >= 2 && cg == 0 && (row & 31) == 0)  // the next step's state into L2 meanwhile

@@ -7,16 +7,16 @@
 // half, so both epilogues run at the same time instead of during the other stream's MMAs.  On a
 // CTA pair a tcgen05.mma.cta_group::2 with M = 256 takes A rows [0, 128) from the leader's shared
 // memory and [128, 256) from the peer's, and B columns [0, N/2) / [N/2, N) likewise: each SM holds
-// half of every W_l N-half (32 KB), so two weight buffers fit beside the A tiles and the next
-// weight load runs under the current MMA, and the two tile streams can run one after the other
+// half of every W_l N-half (32 KB), so a ring of weight buffers fits beside the A tiles and the
+// next weight load runs under the current MMA, and the two tile streams can run one after the other
 // (stream 0's epilogue under stream 1's MMAs and vice versa).
 //
 // Work unit: pair-iteration pi = 512 samples = 4 tiles; stream s, CTA rank r owns tile 4 pi + 2 s + r
 // (TMEM lanes = its 128 samples).  Per layer l the leader issues, for (s, h) = (0,0) (0,1) (1,0)
 // (1,1): 16 MMAs M = 256, N = 128 (output features [128 h, 128 h + 128)), K = 256, into TMEM
-// columns [256 s + 128 h, +128) of both CTAs.  W buffer h holds this CTA's rows of W_l piece h for
-// both streams (loaded once per layer, after stream 1's piece-h MMAs of the previous layer retired),
-// so the next layer's pieces load while stream 1 finishes and stream 0's epilogue runs.  Same math, rounding and outputs as k_tc_fwd2 /
+// columns [256 s + 128 h, +128) of both CTAs.  Each piece is loaded once per layer for both
+// streams, as two K-halves through the ring of F3_WRING buffers (below), so the next layer's
+// weights load while stream 1 finishes and stream 0's epilogue runs.  Same math, rounding and outputs as k_tc_fwd2 /
 // k_tc_mlp MODE 1 (ray-chunk sums of M, h_l images to the h stash, swish'(z_l) / z_{L-1} to the
 // s2 stash).
 //   warps 0-7: stream 0 epilogue, warps 8-15: stream 1 (thread = sample row x column half)
@@ -27,7 +27,7 @@
 // Barriers (per CTA unless noted):
 //   w_full[b]   leader only: its own half loaded (expect_tx) + the peer's half loaded (remote arrive)
 //   w_loc[b]    peer only: its own half loaded
-//   w_free[b]   stream 1's MMAs on buffer b retired (multicast commit to both CTAs)
+//   w_free[b]   stream 1's MMAs on ring buffer b retired (multicast commit to both CTAs)
 //   a_full[s]   leader only: A_s written by both CTAs' stream-s epilogues (1 local + 1 remote arrive)
 //   a_rdy[s]    A_s written by this CTA's epilogue (for its stash store thread)
 //   acc_full[s] stream s's layer retired (multicast commit) and this CTA's stash store read A_s
