@@ -28,6 +28,12 @@ namespace dinr {
 #ifndef B3_WRING
 #define B3_WRING 5
 #endif
+// 1: the delta store of a stream-layer starts with K-blocks 0 and 2 (the first half of every epilogue
+// thread's columns) as soon as the epilogue has written them, so the copy that the next layer's
+// epilogue waits for is half as long; 0: one 64 KB copy after the whole epilogue
+#ifndef B3_SPLIT
+#define B3_SPLIT 1
+#endif
 struct Bwd3Layout {
   static constexpr int H = 256;
   static constexpr int NT = 512 + 128;
@@ -57,7 +63,8 @@ __global__ void __launch_bounds__(Bwd3Layout::NT, 1) k_tc_bwd3(TcParams p, int n
   uint64_t *bars = reinterpret_cast<uint64_t *>(red + 2 * 8 * (H + 1));
   uint64_t *w_full = bars, *w_loc = bars + NWB, *w_free = bars + 2 * NWB;  // [NWB] each
   uint64_t *a_full = bars + 3 * NWB, *a_rdy = a_full + 2, *acc_full = a_full + 4;  // [2] each
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(a_full + 6);
+  uint64_t *h_rdy = a_full + 6;                                                    // [2]
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(a_full + 8);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t rank = cluster_ctarank();
@@ -72,6 +79,7 @@ __global__ void __launch_bounds__(Bwd3Layout::NT, 1) k_tc_bwd3(TcParams p, int n
       mbar_init(&a_full[i], 2);
       mbar_init(&a_rdy[i], 1);
       mbar_init(&acc_full[i], 2);
+      mbar_init(&h_rdy[i], 8);  // one arrival per epilogue warp of the stream
     }
     fence_mbar_init();
   }
@@ -164,15 +172,32 @@ __global__ void __launch_bounds__(Bwd3Layout::NT, 1) k_tc_bwd3(TcParams p, int n
     }
   } else if (tid == 576) {
     // ============================================================ delta-stash stores (both CTAs)
-    uint32_t rph[2] = {0, 0};
+    uint32_t rph[2] = {0, 0}, hph[2] = {0, 0};
+    constexpr uint32_t KB = A_BYTES / 4;  // one 64-column K-block of the image
     for (int64_t pi = cl; pi < n_iter; pi += ncl) {
       for (int l = L - 1; l >= 0; --l) {
         for (int s = 0; s < 2; ++s) {
+          const int64_t tile = 4 * pi + 2 * s + rank;
+          uint8_t *dst = p.dstash + ((size_t)l * p.n_tiles + tile) * A_BYTES;
+          const uint8_t *src = sA0 + s * A_BYTES;
+#if B3_SPLIT
+          mbar_wait_long(&h_rdy[s], hph[s]);
+          hph[s] ^= 1;
+#ifndef DINR_DBG_K3_NOSTORE
+          bulk_s2g(dst, src, KB);
+          bulk_s2g(dst + 2 * KB, src + 2 * KB, KB);
+          bulk_commit();
+#endif
+#endif
           mbar_wait_long(&a_rdy[s], rph[s]);
           rph[s] ^= 1;
-          const int64_t tile = 4 * pi + 2 * s + rank;
 #ifndef DINR_DBG_K3_NOSTORE  // timing experiment only (the dW GEMM then reads a stale delta stash)
-          bulk_s2g(p.dstash + ((size_t)l * p.n_tiles + tile) * A_BYTES, sA0 + s * A_BYTES, A_BYTES);
+#if B3_SPLIT
+          bulk_s2g(dst + KB, src + KB, KB);
+          bulk_s2g(dst + 3 * KB, src + 3 * KB, KB);
+#else
+          bulk_s2g(dst, src, A_BYTES);
+#endif
           bulk_commit();
           bulk_wait_read_all();
 #endif
@@ -196,6 +221,13 @@ __global__ void __launch_bounds__(Bwd3Layout::NT, 1) k_tc_bwd3(TcParams p, int n
     // A_s written -> this CTA's delta store and (unless it is delta_0, which no MMA reads) the
     // pair MMA.  delta_0 must not arrive on a_full: the MMA thread never waits for it, and the next
     // iteration's top-layer hand-off could otherwise complete a second phase before it looks.
+    // K-blocks 0 and 2 of A_s written (every thread's first four 16-column chunks) -> the delta
+    // store may start on them
+    [[maybe_unused]] auto half_off = [&]() {
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&h_rdy[s]);
+    };
     auto hand_off = [&](bool to_mma) {
       fence_proxy_async_smem();
       asm volatile("bar.sync %0, 256;" ::"r"(1 + s) : "memory");
@@ -265,6 +297,9 @@ __global__ void __launch_bounds__(Bwd3Layout::NT, 1) k_tc_bwd3(TcParams p, int n
           }
           st_shared_v4(a_base + sw128_offset(row, c16 * 16, 128), w8[0], w8[1], w8[2], w8[3]);
           st_shared_v4(a_base + sw128_offset(row, c16 * 16 + 8, 128), w8[4], w8[5], w8[6], w8[7]);
+#if B3_SPLIT
+          if (k == NCB - 1) half_off();
+#endif
         }
         if (cg == 0) {
           float us = u_row;
@@ -309,6 +344,9 @@ __global__ void __launch_bounds__(Bwd3Layout::NT, 1) k_tc_bwd3(TcParams p, int n
           }
           st_shared_v4(a_base + sw128_offset(row, c16 * 16, 128), w8[0], w8[1], w8[2], w8[3]);
           st_shared_v4(a_base + sw128_offset(row, c16 * 16 + 8, 128), w8[4], w8[5], w8[6], w8[7]);
+#if B3_SPLIT
+          if (k == NCB - 1) half_off();
+#endif
           if (k + NCB < 2 * NCB)  // NCB chunks ahead, into the registers chunk k just released
             ld_global_v8_hint(zsrc + (size_t)(c16 + NCB) * 128 * 32, zq[k + NCB][0], zq[k + NCB][1], pol_z);
         }
