@@ -34,6 +34,12 @@ namespace dinr {
 #ifndef B3_SPLIT
 #define B3_SPLIT 1
 #endif
+// 1 (with B3_SPLIT): the two column halves of a stream interleave their 16-column chunks (thread
+// column half cg takes chunks 2k + cg), so the K-blocks of A_s complete one after another and each
+// is copied as soon as it is written: the copy the next layer waits for is one 16 KB K-block
+#ifndef B3_QSPLIT
+#define B3_QSPLIT 1
+#endif
 struct Bwd3Layout {
   static constexpr int H = 256;
   static constexpr int NT = 512 + 128;
@@ -63,8 +69,11 @@ __global__ void __launch_bounds__(Bwd3Layout::NT, 1) k_tc_bwd3(TcParams p, int n
   uint64_t *bars = reinterpret_cast<uint64_t *>(red + 2 * 8 * (H + 1));
   uint64_t *w_full = bars, *w_loc = bars + NWB, *w_free = bars + 2 * NWB;  // [NWB] each
   uint64_t *a_full = bars + 3 * NWB, *a_rdy = a_full + 2, *acc_full = a_full + 4;  // [2] each
-  uint64_t *h_rdy = a_full + 6;                                                    // [2]
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(a_full + 8);
+  // h_rdy[s][kb]: K-block kb of A_s written (kb 0..2; with halves only [s][0]: K-blocks 0 and 2).
+  // One barrier per K-block, so none can run more than one phase ahead of the store thread, which
+  // serves the streams in turn.
+  uint64_t *h_rdy = a_full + 6;                                                    // [2][3]
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(a_full + 12);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t rank = cluster_ctarank();
@@ -79,7 +88,7 @@ __global__ void __launch_bounds__(Bwd3Layout::NT, 1) k_tc_bwd3(TcParams p, int n
       mbar_init(&a_full[i], 2);
       mbar_init(&a_rdy[i], 1);
       mbar_init(&acc_full[i], 2);
-      mbar_init(&h_rdy[i], 8);  // one arrival per epilogue warp of the stream
+      for (int kb = 0; kb < 3; ++kb) mbar_init(&h_rdy[i * 3 + kb], 8);  // one arrival per epilogue warp of the stream
     }
     fence_mbar_init();
   }
@@ -172,7 +181,7 @@ __global__ void __launch_bounds__(Bwd3Layout::NT, 1) k_tc_bwd3(TcParams p, int n
     }
   } else if (tid == 576) {
     // ============================================================ delta-stash stores (both CTAs)
-    uint32_t rph[2] = {0, 0}, hph[2] = {0, 0};
+    uint32_t rph[2] = {0, 0}, hph[2] = {0, 0};  // (every h_rdy[s][kb] completes once per store: one parity per stream)
     constexpr uint32_t KB = A_BYTES / 4;  // one 64-column K-block of the image
     for (int64_t pi = cl; pi < n_iter; pi += ncl) {
       for (int l = L - 1; l >= 0; --l) {
@@ -180,8 +189,17 @@ __global__ void __launch_bounds__(Bwd3Layout::NT, 1) k_tc_bwd3(TcParams p, int n
           const int64_t tile = 4 * pi + 2 * s + rank;
           uint8_t *dst = p.dstash + ((size_t)l * p.n_tiles + tile) * A_BYTES;
           const uint8_t *src = sA0 + s * A_BYTES;
-#if B3_SPLIT
-          mbar_wait_long(&h_rdy[s], hph[s]);
+#if B3_SPLIT && B3_QSPLIT
+          for (int kb = 0; kb < 3; ++kb) {  // K-blocks 0, 1, 2 as the epilogue completes them
+            mbar_wait_long(&h_rdy[s * 3 + kb], hph[s]);
+#ifndef DINR_DBG_K3_NOSTORE
+            bulk_s2g(dst + kb * KB, src + kb * KB, KB);
+            bulk_commit();
+#endif
+          }
+          hph[s] ^= 1;
+#elif B3_SPLIT
+          mbar_wait_long(&h_rdy[s * 3], hph[s]);
           hph[s] ^= 1;
 #ifndef DINR_DBG_K3_NOSTORE
           bulk_s2g(dst, src, KB);
@@ -192,7 +210,9 @@ __global__ void __launch_bounds__(Bwd3Layout::NT, 1) k_tc_bwd3(TcParams p, int n
           mbar_wait_long(&a_rdy[s], rph[s]);
           rph[s] ^= 1;
 #ifndef DINR_DBG_K3_NOSTORE  // timing experiment only (the dW GEMM then reads a stale delta stash)
-#if B3_SPLIT
+#if B3_SPLIT && B3_QSPLIT
+          bulk_s2g(dst + 3 * KB, src + 3 * KB, KB);
+#elif B3_SPLIT
           bulk_s2g(dst + KB, src + KB, KB);
           bulk_s2g(dst + 3 * KB, src + 3 * KB, KB);
 #else
@@ -212,6 +232,10 @@ __global__ void __launch_bounds__(Bwd3Layout::NT, 1) k_tc_bwd3(TcParams p, int n
     const int s = tid >> 8, wt = tid & 255;
     const int row = wt & 127, cg = wt >> 7;
     const int cb_lo = cg * NCB;
+    // the thread's k-th 16-column chunk
+    auto c16_of = [&](int k) { return B3_SPLIT && B3_QSPLIT ? 2 * k + cg : cb_lo * 2 + k; };
+    // K-block written: 0 and 2 at k = NCB - 1 (halves), or K-block (k - 1) / 2 at odd k (interleaved)
+    auto kblock_done = [&](int k) { return B3_SPLIT && (B3_QSPLIT ? ((k & 1) && k < 2 * NCB - 1) : k == NCB - 1); };
     const uint32_t a_base = smem_u32(sA0) + s * A_BYTES;
     const uint32_t tmem_row = tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(s * 256);
     const uint32_t a_full_leader = mapa_shared(smem_u32(&a_full[s]), 0);
@@ -223,10 +247,10 @@ __global__ void __launch_bounds__(Bwd3Layout::NT, 1) k_tc_bwd3(TcParams p, int n
     // iteration's top-layer hand-off could otherwise complete a second phase before it looks.
     // K-blocks 0 and 2 of A_s written (every thread's first four 16-column chunks) -> the delta
     // store may start on them
-    [[maybe_unused]] auto half_off = [&]() {
+    [[maybe_unused]] auto half_off = [&](int kb) {
       fence_proxy_async_smem();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&h_rdy[s]);
+      if (lane == 0) mbar_arrive(&h_rdy[s * 3 + kb]);
     };
     auto hand_off = [&](bool to_mma) {
       fence_proxy_async_smem();
@@ -249,7 +273,7 @@ __global__ void __launch_bounds__(Bwd3Layout::NT, 1) k_tc_bwd3(TcParams p, int n
       {
         const uint8_t *zsrc = p.zstash + (((size_t)(L - 1) * p.n_tiles + tile) * (H / 16) * 128 + row) * 32;
         uint4 zt[2][2];
-        ld_global_v8_hint(zsrc + (size_t)(cb_lo * 2) * 128 * 32, zt[0][0], zt[0][1], pol_z);
+        ld_global_v8_hint(zsrc + (size_t)c16_of(0) * 128 * 32, zt[0][0], zt[0][1], pol_z);
         if (a_busy) {
           mbar_wait_long(&acc_full[s], accph);  // CTA scope: TMEM + own smem only
           accph ^= 1;
@@ -257,9 +281,9 @@ __global__ void __launch_bounds__(Bwd3Layout::NT, 1) k_tc_bwd3(TcParams p, int n
         a_busy = true;
 #pragma unroll
         for (int k = 0; k < 2 * NCB; ++k) {
-          const int c16 = cb_lo * 2 + k;
+          const int c16 = c16_of(k);
           if (k + 1 < 2 * NCB)
-            ld_global_v8_hint(zsrc + (size_t)(c16 + 1) * 128 * 32, zt[(k + 1) & 1][0], zt[(k + 1) & 1][1], pol_z);
+            ld_global_v8_hint(zsrc + (size_t)c16_of(k + 1) * 128 * 32, zt[(k + 1) & 1][0], zt[(k + 1) & 1][1], pol_z);
           float z[16];
 #pragma unroll
           for (int q = 0; q < 2; ++q) {
@@ -297,9 +321,7 @@ __global__ void __launch_bounds__(Bwd3Layout::NT, 1) k_tc_bwd3(TcParams p, int n
           }
           st_shared_v4(a_base + sw128_offset(row, c16 * 16, 128), w8[0], w8[1], w8[2], w8[3]);
           st_shared_v4(a_base + sw128_offset(row, c16 * 16 + 8, 128), w8[4], w8[5], w8[6], w8[7]);
-#if B3_SPLIT
-          if (k == NCB - 1) half_off();
-#endif
+          if (kblock_done(k)) half_off(B3_QSPLIT ? (k >> 1) : 0);
         }
         if (cg == 0) {
           float us = u_row;
@@ -319,7 +341,7 @@ __global__ void __launch_bounds__(Bwd3Layout::NT, 1) k_tc_bwd3(TcParams p, int n
 #define ld_global_v8_hint(...) (void)0
 #endif
 #pragma unroll
-        for (int k = 0; k < NCB; ++k) ld_global_v8_hint(zsrc + (size_t)(cb_lo * 2 + k) * 128 * 32, zq[k][0], zq[k][1], pol_z);
+        for (int k = 0; k < NCB; ++k) ld_global_v8_hint(zsrc + (size_t)c16_of(k) * 128 * 32, zq[k][0], zq[k][1], pol_z);
         if (l >= 2 && cg == 0 && (row & 31) == 0)  // the next step's state into L2 meanwhile
           bulk_prefetch_l2(p.zstash + ((size_t)(l - 2) * p.n_tiles + tile) * kZTile + (size_t)(row >> 5) * (kZTile / 4),
                            kZTile / 4);
@@ -328,7 +350,7 @@ __global__ void __launch_bounds__(Bwd3Layout::NT, 1) k_tc_bwd3(TcParams p, int n
         tc_fence_after();
 #pragma unroll
         for (int k = 0; k < 2 * NCB; ++k) {
-          const int c16 = cb_lo * 2 + k;
+          const int c16 = c16_of(k);
           uint32_t v[16];
           tmem_ld16(tmem_row + c16 * 16, v);
           tmem_wait_ld();
@@ -344,11 +366,9 @@ __global__ void __launch_bounds__(Bwd3Layout::NT, 1) k_tc_bwd3(TcParams p, int n
           }
           st_shared_v4(a_base + sw128_offset(row, c16 * 16, 128), w8[0], w8[1], w8[2], w8[3]);
           st_shared_v4(a_base + sw128_offset(row, c16 * 16 + 8, 128), w8[4], w8[5], w8[6], w8[7]);
-#if B3_SPLIT
-          if (k == NCB - 1) half_off();
-#endif
+          if (kblock_done(k)) half_off(B3_QSPLIT ? (k >> 1) : 0);
           if (k + NCB < 2 * NCB)  // NCB chunks ahead, into the registers chunk k just released
-            ld_global_v8_hint(zsrc + (size_t)(c16 + NCB) * 128 * 32, zq[k + NCB][0], zq[k + NCB][1], pol_z);
+            ld_global_v8_hint(zsrc + (size_t)c16_of(k + NCB) * 128 * 32, zq[k + NCB][0], zq[k + NCB][1], pol_z);
         }
         tc_fence_before();
         hand_off(l >= 2);
@@ -365,13 +385,15 @@ __global__ void __launch_bounds__(Bwd3Layout::NT, 1) k_tc_bwd3(TcParams p, int n
     const int s = tid >> 8, wt = tid & 255, cg = wt >> 7, w8 = wt >> 5;
     if (lane < 16)
 #pragma unroll
-      for (int k = 0; k < 2 * NCB; ++k) red[(s * 8 + w8) * (H + 1) + (cg * NCB * 2 + k) * 16 + lane] = head_acc[k];
+      for (int k = 0; k < 2 * NCB; ++k)
+        red[(s * 8 + w8) * (H + 1) + (B3_SPLIT && B3_QSPLIT ? 2 * k + cg : cg * NCB * 2 + k) * 16 + lane] = head_acc[k];
     if (lane == 0) red[(s * 8 + w8) * (H + 1) + H] = bo_acc;  // (zero for column-half-1 warps)
   }
   __syncthreads();
   for (int k = tid; k <= H; k += LY::NT) {
     float acc = 0.f;
-    const int w0 = (k < H && k >= H / 2) ? 4 : 0;
+    // the warps of the column half that holds column k (chunks 2k' + cg when interleaved)
+    const int w0 = (k < H && (B3_SPLIT && B3_QSPLIT ? ((k >> 4) & 1) : k >= H / 2)) ? 4 : 0;
     for (int s = 0; s < 2; ++s)
       for (int w = w0; w < w0 + 4; ++w) acc += red[(s * 8 + w) * (H + 1) + k];
     p.head_part[(size_t)blockIdx.x * (H + 1) + k] = acc;
