@@ -83,3 +83,20 @@ def test_world_mismatch_fails_loudly():
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2"], capture_output=True,
                          text=True, timeout=300, cwd=ROOT, env=env)
     assert out.returncode != 0 and "WORLD_SIZE" in out.stderr
+
+
+def test_profiled_traffic_lookup():
+    """roofline.traffic comes from the committed ncu --set full captures (profiles/traffic.json, one
+    entry per workload): the dominant kernel of each bench workload has a capture, and a workload
+    or kernel class without one reads as None (the line then says traffic: null)."""
+    sys.path.insert(0, ROOT)
+    import bench
+
+    with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+        tr = json.load(fh)["workloads"]
+    assert bench.profiled_traffic("cone4d2048", "forward", 0) in tr["cone4d2048"]["kernels"].values()
+    assert bench.profiled_traffic("cone4d2048", "backward", 0) in tr["cone4d2048"]["kernels"].values()
+    assert bench.profiled_traffic("fan512", "backward", 2) in tr["fan512"]["kernels"].values()
+    assert bench.profiled_traffic("cone4d2048", "forward", 0) > 1e10  # the stash writes: ~21 GB per launch
+    assert bench.profiled_traffic("no-such-workload", "forward", 0) is None
+    assert bench.profiled_traffic("cone4d2048", "no-such-class", 0) is None
