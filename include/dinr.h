@@ -96,7 +96,9 @@ typedef struct {
 
 /* DINR field network: GRFF with n_freq = C frequencies (width H = 2C), L =
  * n_layers FC(H->H)+Swish layers, FC head H->1 times mu0 (applied once, R6).
- * Supported on the BF16 path: H in {64, 128, 256}, 1 <= L <= 64; FP32_VERIFY: any even H <= 256.
+ * Supported on the BF16 path: H in {64, 128, 256}, 1 <= L <= 64 (L <= 27 at H = 256, where every
+ * layer's bias sits in the tensor-core kernels' shared memory; DINR_EINVAL beyond); FP32_VERIFY: any
+ * even H <= 256.
  * Accuracy envelope of the BF16 path (bf16 tensor-core operands, fp32 accumulation and epilogue):
  * against the fp64 oracle, projections within 2e-3 and gradients within 1e-2 (relative L-inf per
  * parameter tensor, R23) for L <= 3 at H = 64, L <= 4 at H = 128 and L <= 6 at H = 256

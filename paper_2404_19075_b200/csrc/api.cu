@@ -220,7 +220,8 @@ size_t plan_layout(dinr_ctx *c, int64_t n, bool train, bool host_io, Plan &pl, v
   // (experiment, off by default: measured no faster -- the forward saves its writes but K3 and the
   // dW GEMM redo the MUFU work)
   static const bool zall_on = std::getenv("DINR_ZALL") != nullptr;
-  const bool zall_path = train && !simt && !use_fused(c) && c->H == 256 && fwd3_on() && zall_on;
+  const bool zall_path = train && !simt && !use_fused(c) && c->H == 256 && fwd3_on() && zall_on &&
+                         Fwd3Layout::smem_bytes(c->L) <= kMaxSmem;
   if (zall_path) pl.ks0 = pl.ks1 = pl.ksplit = (int)std::max<int64_t>(1, std::min<int64_t>(pl.n_tiles, c->sm_count / c->L));
   static const bool split_feat0 = std::getenv("DINR_SPLIT_FEAT0") != nullptr;
   const bool sfeat0 = split_feat0 && !zall_path && train && !simt && !use_fused(c) && c->L >= 2;
@@ -476,8 +477,8 @@ dinr_status launch_tc_mlp(dinr_ctx *c, const Plan &pl, int mode, cudaStream_t st
     if (s) return s;
     Launch L_(c, T_BWD, st);
     k_tc_mlp<H, 2><<<pl.grid_tc, kTcThreads, smem, st>>>(p);
-  } else if (mode == 1 && H == 256 && fwd3_on()) {
-    // CTA pairs (cta_group::2, M = 256), two tile streams, W_l double-buffered (k_tc_fwd3.cuh)
+  } else if (mode == 1 && H == 256 && fwd3_on() && Fwd3Layout::smem_bytes(c->L) <= kMaxSmem) {
+    // CTA pairs (cta_group::2, M = 256), two tile streams, W_l through a ring of K-half buffers (k_tc_fwd3.cuh)
     const size_t sm3 = Fwd3Layout::smem_bytes(c->L);
     dinr_status s = set_smem(c, k_tc_fwd3, sm3);
     if (s) return s;
@@ -520,7 +521,7 @@ dinr_status launch_tc_mlp(dinr_ctx *c, const Plan &pl, int mode, cudaStream_t st
                    2 * tot[9] / it, tot[10] / it, 2 * tot[11] / it, tot[12] / it, tot[13] / it);
     }
 #endif
-  } else if (mode == 1 && H == 256 && !std::getenv("DINR_NO_FWD2")) {
+  } else if (mode == 1 && H == 256 && !std::getenv("DINR_NO_FWD2") && Fwd2Layout::smem_bytes(c->L) <= kMaxSmem) {
     // two tile streams per CTA, W_l streamed in N-halves (k_tc_fwd2.cuh)
     const size_t sm2 = Fwd2Layout::smem_bytes(c->L);
     dinr_status s = set_smem(c, k_tc_fwd2, sm2);
@@ -1057,6 +1058,9 @@ dinr_status dinr_set_field_weights(dinr_ctx *c, const dinr_field_desc *f, const 
       return fail(c, DINR_EINVAL, "BF16 path supports width 64, 128 or 256");
     if (c->geom.samples_per_ray % 32)
       return fail(c, DINR_EINVAL, "the BF16 path needs samples_per_ray a multiple of 32 (FP32_VERIFY accepts any)");
+    // at H = 256 every layer's bias sits in the tensor-core kernels' shared memory
+    if (f->width == 256 && TcLayout<256>::smem_bytes(f->n_layers, false) > kMaxSmem)
+      return fail(c, DINR_EINVAL, "the BF16 path supports n_layers <= 27 at width 256");
   } else if (f->precision == DINR_FP32_VERIFY) {
     if (f->width > kMaxH || f->width % 2) return fail(c, DINR_EINVAL, "FP32_VERIFY supports width <= 256");
   } else {

@@ -80,3 +80,49 @@ def test_split_path_multi_iteration_parity(dev, O, L):
         off += m
     assert max(errs) <= 1e-2, errs
     assert abs(got[-1] - ref[-1]) <= 1e-2 * abs(ref[-1]), (got[-1], ref[-1])  # the loss slot
+
+
+def test_deep_h256_falls_back_and_bounds(dev):
+    """At H = 256 the forward kernel is chosen by shared-memory fit: L = 12 runs k_tc_fwd3, L = 16
+    k_tc_fwd2 (k_tc_fwd3's K-half weight ring leaves room for the biases of 12 layers), L = 27 the
+    one-tile k_tc_mlp; L = 28 is refused at dinr_set_field_weights (include/dinr.h).  Deep networks
+    are outside the bf16 accuracy envelope, so this checks the launch, the status and a finite,
+    batch-consistent result: the loss is the batch mean, so the gradient of a batch equals half the
+    sum of its two equal halves' gradients (accumulate mode) to fp32 reduction-order precision."""
+    name = "cone512"
+    g = synth.geometry(name, n_s=32)
+    th, t = synth.views(name, n_s=32)
+    for L in (12, 16, 27):
+        f = synth.field(name, L=L)
+        B = synth.grff_matrix(f["C"], f["sigma_t"], f["sigma_s"], seed=21)
+        prm = synth.init_params(f["C"], f["L"], seed=22, head_bias=0.5)
+        ctx = D.create(0)
+        try:
+            D.set_geometry(ctx, g, th, t)
+            D.set_field_weights(ctx, f, torch.tensor(B, device=dev), torch.tensor(prm, device=dev))
+            n = 24
+            idx = torch.tensor(synth.pixel_batch(name, n, seed=23, n_s=32), device=dev)
+            y = torch.full((n,), 0.5, device=dev)
+            P = synth.param_count(f["C"], f["L"])
+            g_all = torch.zeros(P + 1, device=dev)
+            D.project_and_grad(ctx, idx, y, g_all)
+            g_half = torch.zeros(P + 1, device=dev)
+            D.project_and_grad(ctx, idx[: n // 2], y[: n // 2], g_half)
+            D.project_and_grad(ctx, idx[n // 2:], y[n // 2:], g_half, accumulate=True)
+            torch.cuda.synchronize()
+            assert D.get_device_status(ctx) == 0
+        finally:
+            D.destroy(ctx)
+        a, b = g_all[:-1].cpu().numpy(), 0.5 * g_half[:-1].cpu().numpy()
+        assert np.all(np.isfinite(a)) and np.max(np.abs(a)) > 0, L
+        assert rel_linf(b, a) <= 1e-4, (L, rel_linf(b, a))
+    f = synth.field(name, L=28)
+    ctx = D.create(0)
+    try:
+        D.set_geometry(ctx, g, th, t)
+        B = synth.grff_matrix(f["C"], f["sigma_t"], f["sigma_s"], seed=21)
+        prm = synth.init_params(f["C"], f["L"], seed=22)
+        with pytest.raises(D.DinrError):
+            D.set_field_weights(ctx, f, torch.tensor(B, device=dev), torch.tensor(prm, device=dev))
+    finally:
+        D.destroy(ctx)
