@@ -84,8 +84,9 @@ def test_split_path_multi_iteration_parity(dev, O, L):
 
 def test_deep_h256_falls_back_and_bounds(dev):
     """At H = 256 the forward kernel is chosen by shared-memory fit: L = 12 runs k_tc_fwd3, L = 16
-    k_tc_fwd2 (k_tc_fwd3's K-half weight ring leaves room for the biases of 12 layers), L = 27 the
-    one-tile k_tc_mlp; L = 28 is refused at dinr_set_field_weights (include/dinr.h).  Deep networks
+    and L = 27 k_tc_fwd2 (k_tc_fwd3's K-half weight ring leaves room for the biases of 12 layers);
+    L = 28 is refused at dinr_set_field_weights (the forward-only k_tc_mlp no longer fits;
+    include/dinr.h).  Deep networks
     are outside the bf16 accuracy envelope, so this checks the launch, the status and a finite,
     batch-consistent result: the loss is the batch mean, so the gradient of a batch equals half the
     sum of its two equal halves' gradients (accumulate mode) to fp32 reduction-order precision."""
