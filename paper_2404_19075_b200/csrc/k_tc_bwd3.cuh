@@ -21,6 +21,11 @@
 
 namespace dinr {
 
+// stash copies stream through L2 (evict_first): they are read back by a later kernel, 21 GB later
+#ifndef STASH_S2G
+#define STASH_S2G(d, s_, n) bulk_s2g_hint(d, s_, n, policy_evict_first())
+#endif
+
 // The W blocks move through a ring of B3_WRING K-half buffers (rows [128 kh, +128) of this CTA's
 // 64-column block of piece h, 16 KB): K-half j of the kernel's sequence (layer, piece, K-half; both
 // streams use it) in buffer j mod B3_WRING, so the next layer's first K-half loads while the
@@ -193,7 +198,7 @@ __global__ void __launch_bounds__(Bwd3Layout::NT, 1) k_tc_bwd3(TcParams p, int n
           for (int kb = 0; kb < 3; ++kb) {  // K-blocks 0, 1, 2 as the epilogue completes them
             mbar_wait_long(&h_rdy[s * 3 + kb], hph[s]);
 #ifndef DINR_DBG_K3_NOSTORE
-            bulk_s2g(dst + kb * KB, src + kb * KB, KB);
+            STASH_S2G(dst + kb * KB, src + kb * KB, KB);
             bulk_commit();
 #endif
           }
@@ -202,8 +207,8 @@ __global__ void __launch_bounds__(Bwd3Layout::NT, 1) k_tc_bwd3(TcParams p, int n
           mbar_wait_long(&h_rdy[s * 3], hph[s]);
           hph[s] ^= 1;
 #ifndef DINR_DBG_K3_NOSTORE
-          bulk_s2g(dst, src, KB);
-          bulk_s2g(dst + 2 * KB, src + 2 * KB, KB);
+          STASH_S2G(dst, src, KB);
+          STASH_S2G(dst + 2 * KB, src + 2 * KB, KB);
           bulk_commit();
 #endif
 #endif
@@ -211,12 +216,12 @@ __global__ void __launch_bounds__(Bwd3Layout::NT, 1) k_tc_bwd3(TcParams p, int n
           rph[s] ^= 1;
 #ifndef DINR_DBG_K3_NOSTORE  // timing experiment only (the dW GEMM then reads a stale delta stash)
 #if B3_SPLIT && B3_QSPLIT
-          bulk_s2g(dst + 3 * KB, src + 3 * KB, KB);
+          STASH_S2G(dst + 3 * KB, src + 3 * KB, KB);
 #elif B3_SPLIT
-          bulk_s2g(dst + KB, src + KB, KB);
-          bulk_s2g(dst + 3 * KB, src + 3 * KB, KB);
+          STASH_S2G(dst + KB, src + KB, KB);
+          STASH_S2G(dst + 3 * KB, src + 3 * KB, KB);
 #else
-          bulk_s2g(dst, src, A_BYTES);
+          STASH_S2G(dst, src, A_BYTES);
 #endif
           bulk_commit();
           bulk_wait_read_all();

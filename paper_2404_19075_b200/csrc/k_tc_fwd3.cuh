@@ -39,6 +39,11 @@
 
 namespace dinr {
 
+// stash copies stream through L2 (evict_first): they are read back by a later kernel, 21 GB later
+#ifndef STASH_S2G
+#define STASH_S2G(d, s_, n) bulk_s2g_hint(d, s_, n, policy_evict_first())
+#endif
+
 #ifdef DINR_PHASES
 #define F3_T0() const long long _t0 = clock64()
 #define F3_ACC(v) (v) += (unsigned long long)(clock64() - _t0)
@@ -248,7 +253,7 @@ __global__ void __launch_bounds__(Fwd3Layout::NT, 1) k_tc_fwd3(TcParams p) {
           const int64_t tile = 4 * pi + 2 * s + rank;
           // layer l's input for the dW GEMM (l = 0: the GRFF features, unless the dW GEMM recomputes them)
           if (!p.zall && (l > 0 || p.stash_feat)) {
-            bulk_s2g(p.hstash + ((size_t)l * p.n_tiles + tile) * A_BYTES, sA0 + s * A_BYTES, A_BYTES);
+            STASH_S2G(p.hstash + ((size_t)l * p.n_tiles + tile) * A_BYTES, sA0 + s * A_BYTES, A_BYTES);
             bulk_commit();
             F3_T0();
             bulk_wait_read_all();
