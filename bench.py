@@ -459,6 +459,20 @@ def main():
             achieved = work / avg_s / 1e9
             roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                     "traffic": profiled_traffic(name, dom, path_kind), "kernel": dom, "peak_source": f"{peak_src} HBM copy"}
+        # split path (H = 256): each of K2, K3, K5 moves 4 L H bytes of stash per sample (DESIGN.md
+        # section 11: h and s2 written / s2 read and delta written / h and delta read, 2 H bytes per
+        # sample and layer each); their HBM view beside the tensor one
+        stash = None
+        if path_kind == 0 and not os.environ.get("DINR_ZALL"):
+            bps = 4.0 * L * H
+            stash = {"bytes_per_sample": bps, "peak_gbs": hbm, "peak_source": f"{peak_src} HBM copy",
+                     "achieved_gbs": {}, "frac": {}}
+            for k in ("forward", "backward", "dw"):
+                ms_k2, n_k2 = ktimes.get(k, (0.0, 0))
+                if n_k2 > 0 and ms_k2 > 0:
+                    gbs = bps * nsamp / ((ms_k2 / n_k2) / 1e3) / 1e9
+                    stash["achieved_gbs"][k] = gbs
+                    stash["frac"][k] = gbs / hbm
         step_tflops = value * fps / 1e12
         # configs with small H can be bound by the MUFU (tanh per activation, sin/cos per
         # frequency: L*H + 2C per sample forward) or the FP32/FMA pipe (~10 epilogue ops per
@@ -490,6 +504,7 @@ def main():
                               "frac_burst": step_tflops / tf_burst,
                               "frac_sustained": step_tflops / tf_sust if tf_sust else None},
             "binding_roofline": binding,
+            "stash_roofline": stash,
             "kernel_ms_per_step": {k: v[0] / args.steps for k, v in ktimes.items()},
             "cpu_baseline": ({"value": base_rate, "unit": UNIT, "cores": cores(), "kind": "oracle",
                               "sample": f"{base_px} pixels ({base_px * S * ns} samples) of {name}, "
