@@ -65,6 +65,10 @@ def test_our_arm_line():
     for k in ("sm_mhz", "sm_max_mhz", "reasons"):
         assert k in d["clocks"], k
     assert d["replicas_equal"] is True
+    st = d["stash_roofline"]  # the split path's HBM view: 4 L H bytes per sample for K2, K3, K5
+    assert st["bytes_per_sample"] == 4 * 5 * 256
+    for k in ("forward", "backward", "dw"):
+        assert 0 < st["frac"][k] < 1.2 and abs(st["achieved_gbs"][k] / st["peak_gbs"] - st["frac"][k]) < 1e-9
 
 
 def test_launcher_spawns_one_rank_per_gpu():
