@@ -164,13 +164,20 @@ def oracle_rate(name, budget_s=15.0, max_pixels=1 << 20):
 
 
 def cores():
-    return os.cpu_count() or 1
+    """Threads the oracle's OpenMP loops use: the "cores" of a host timing."""
+    from oracle import oracle as O
+
+    return O.max_threads()
 
 
 # ---------------------------------------------------------------------------- reference arm
 def run_reference(args, rank, world):
     if rank != 0:
         return 0
+    # torch.distributed.run sets OMP_NUM_THREADS=1 for every rank; rank 0 alone runs the oracle
+    # here, on all of the host's cores (set before the oracle's OpenMP runtime starts)
+    if world > 1 and os.environ.get("OMP_NUM_THREADS") == "1":
+        os.environ["OMP_NUM_THREADS"] = str(os.cpu_count() or 1)
     name = args.workload
     g = synth.geometry(name)
     S, ns = g["sub_x"] * g["sub_z"], g["n_s"]
@@ -220,8 +227,9 @@ def free_port():
 def launch_ranks(args):
     """`bench.py --gpus N` run without torchrun: re-execute this script under
     torch.distributed.run, one rank per GPU on this node (the launch the driver uses for N > 1),
-    and return its exit code.  Fails loudly when fewer than N devices are visible."""
-    if not args.launch_dry_run:
+    and return its exit code.  Fails loudly when fewer than N devices are visible (the reference
+    arm runs the oracle on the host: rank 0 alone works, so it needs no device)."""
+    if not args.launch_dry_run and args.impl != "reference":
         import torch
 
         have = torch.cuda.device_count()

@@ -776,3 +776,5 @@ int or_sample_batch(int64_t M, int64_t N, uint64_t seed, int64_t epoch, int64_t 
   }
   return 0;
 }
+
+int or_max_threads(void) { return omp_get_max_threads(); }

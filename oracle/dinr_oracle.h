@@ -168,6 +168,10 @@ int or_sample_batch(int64_t M, int64_t N, uint64_t seed, int64_t epoch, int64_t 
 /* Iterations per epoch: ceil(M N / (world n)). */
 int64_t or_iterations_per_epoch(int64_t M, int64_t N, int world, int64_t n);
 
+/* OpenMP threads the oracle's parallel loops use (omp_get_max_threads; OMP_NUM_THREADS): the
+ * "cores" of a host timing of the oracle.  Not part of the method. */
+int or_max_threads(void);
+
 #ifdef __cplusplus
 }
 #endif

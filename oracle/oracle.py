@@ -70,6 +70,8 @@ def lib():
         _lib = C.CDLL(build())
         d, i64, i32 = C.POINTER(C.c_double), C.c_int64, C.c_int32
         pi64 = C.POINTER(C.c_int64)
+        _lib.or_max_threads.restype = C.c_int
+        _lib.or_max_threads.argtypes = []
         _lib.or_param_count.restype = i64
         _lib.or_param_count.argtypes = [i32, i32]
         _lib.or_rotate_point.argtypes = [C.c_double] * 4 + [d, d]
@@ -352,3 +354,8 @@ def train(g, theta, t, f, B, params, y_src, seed, n, world, iterations, sharding
         losses.append(float(avg[P]))
         prm, m, v = adam_step(prm, avg[:P], m, v, lr0 * decay ** epoch, b1, b2, eps, gi + 1)
     return prm, np.array(losses)
+
+
+def max_threads() -> int:
+    """OpenMP threads the oracle's loops use (for the host timings' "cores")."""
+    return int(lib().or_max_threads())
