@@ -104,3 +104,13 @@ def test_profiled_traffic_lookup():
     assert bench.profiled_traffic("cone4d2048", "forward", 0) > 1e10  # the stash writes: ~21 GB per launch
     assert bench.profiled_traffic("no-such-workload", "forward", 0) is None
     assert bench.profiled_traffic("cone4d2048", "no-such-class", 0) is None
+
+
+def test_reference_arm_under_two_ranks_uses_all_host_cores():
+    """The driver launches the reference arm like ours (torchrun for N > 1): rank 0 alone times the
+    oracle and prints one line, the other rank exits 0; torchrun's OMP_NUM_THREADS=1 must not pin
+    the oracle to one core (the line's cores = the oracle's OpenMP threads)."""
+    d = run_bench("--impl", "reference", "--gpus", "2", "--workload", "parallel64", "--steps", "1", "--warmup", "1",
+                  "--ref-seconds", "2")
+    assert d["impl"] == "reference" and d["n_gpus"] == 2
+    assert d["cpu_baseline"]["cores"] == (os.cpu_count() or 1)
